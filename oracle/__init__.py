@@ -1,0 +1,290 @@
+"""CPU oracle for the Time-Warped Grid hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` legs may import this package.  The product path
+(``paper_1903_07441_b200``) never imports it, and the two share no code: the
+only common dependency is the input generator ``scenes/``.
+
+The arithmetic lives in ``twg_oracle.c`` (plain C, built with
+``-O2 -ffp-contract=off -fno-fast-math``); this module only builds it and
+marshals numpy arrays through ctypes.  ``plan_step`` composes the steps O1-O8
+in the order of Algorithm 1.
+
+Parity unpinned (stated here and in DESIGN.md): the exact smoothed path on
+general scenes (only properties of ``band`` are pinned), the warm-start
+trajectory over many ticks, and the next-waypoint choice.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "twg_oracle.c")
+_LIB = os.path.join(_HERE, "libtwg_oracle.so")
+_lib = None
+
+FREE, OBSTACLE, GOAL = 0, 1, 2
+OK, W_GOAL_SWALLOWED, E_INVALID_ARG, E_OUT_OF_BOUNDS, E_OVERLAPPING, E_INVALID_START, E_NO_PATH = 0, 1, -1, -2, -3, -4, -5
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (no FMA contraction, no fast-math, no FTZ/DAZ)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+               "-Wall", "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB)
+        d, i32, i64, f32 = C.c_double, C.c_int32, C.c_int64, C.c_float
+        P = C.c_void_p
+        L.orc_eq14_lhs.restype = d
+        L.orc_eq14_lhs.argtypes = [d] * 7
+        L.orc_warp_radius.restype = d
+        L.orc_warp_radius.argtypes = [d] * 6
+        L.orc_warp_number.restype = i32
+        L.orc_warp_number.argtypes = [d, d]
+        L.orc_horizon.restype = i32
+        L.orc_horizon.argtypes = [i32, d, d, d, d, i32]
+        L.orc_predict.restype = None
+        L.orc_predict.argtypes = [P, P, P, d, i32, P, P]
+        L.orc_footprint_r2.restype = d
+        L.orc_footprint_r2.argtypes = [P, d]
+        L.orc_stamp_bruteforce.restype = None
+        L.orc_stamp_bruteforce.argtypes = [i32, i32, d, d, d, d, d, d, P]
+        L.orc_stamp_box.restype = None
+        L.orc_stamp_box.argtypes = [i32, i32, d, d, d, d, d, d, P]
+        L.orc_classify.restype = i32
+        L.orc_classify.argtypes = [i32, i32, d, d, d, P, i32, i32, d, d, d, d, i32, P,
+                                   d, P, d, d, d, i32, P, P, P, P]
+        L.orc_init_u32.restype = None
+        L.orc_init_u32.argtypes = [i64, P, P, P, P]
+        L.orc_init_u64.restype = None
+        L.orc_init_u64.argtypes = [i64, P, P]
+        L.orc_relax_f32.restype = i32
+        L.orc_relax_f32.argtypes = [i32, i32, P, P, i32, i32, f32, P]
+        L.orc_relax_f64.restype = i32
+        L.orc_relax_f64.argtypes = [i32, i32, P, P, i32, i32, d, P]
+        L.orc_jacobi_f64.restype = i32
+        L.orc_jacobi_f64.argtypes = [i32, i32, P, P, i32, d, P]
+        L.orc_walk.restype = i32
+        L.orc_walk.argtypes = [i32, i32, P, P, i32, i32, i32, P, P]
+        L.orc_bilerp.restype = f32
+        L.orc_bilerp.argtypes = [i32, i32, P, f32, f32]
+        L.orc_band.restype = None
+        L.orc_band.argtypes = [i32, i32, P, P, i32, P, i32, f32, f32]
+        L.orc_band_sequential.restype = None
+        L.orc_band_sequential.argtypes = [i32, i32, P, P, i32, P, i32, f32, f32]
+        L.orc_resample.restype = i32
+        L.orc_resample.argtypes = [i32, P, i32, P]
+        L.orc_next_waypoint.restype = i32
+        L.orc_next_waypoint.argtypes = [i32, P, P, P]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------- O1, O2
+def eq14_lhs(xr, yr, theta, xo, yo, rx):
+    return lib().orc_eq14_lhs(xr, yr, math.cos(theta), math.sin(theta), xo, yo, rx)
+
+
+def warp_radius(xr, yr, theta, xo, yo):
+    return lib().orc_warp_radius(xr, yr, math.cos(theta), math.sin(theta), xo, yo)
+
+
+def warp_number(rx, w=1.0):
+    return lib().orc_warp_number(rx, w)
+
+
+def horizon(t, speed_r, vx, vy, eps_v=0.05, hmax=20):
+    return lib().orc_horizon(t, speed_r, vx, vy, eps_v, hmax)
+
+
+def predict(x, P, Q, dt, j):
+    x = np.ascontiguousarray(x, np.float64).reshape(4)
+    P = np.ascontiguousarray(P, np.float64).reshape(16)
+    Q = np.ascontiguousarray(Q, np.float64).reshape(16)
+    xo = np.zeros(4)
+    Po = np.zeros(16)
+    lib().orc_predict(_p(x), _p(P), _p(Q), dt, int(j), _p(xo), _p(Po))
+    return xo, Po.reshape(4, 4)
+
+
+def footprint_r2(P, rs):
+    P = np.ascontiguousarray(P, np.float64).reshape(16)
+    return lib().orc_footprint_r2(_p(P), rs)
+
+
+def stamp_disk(W, H, cs, ox, oy, xp, yp, R2, brute=True):
+    m = np.zeros((H, W), np.uint8)
+    f = lib().orc_stamp_bruteforce if brute else lib().orc_stamp_box
+    f(W, H, cs, ox, oy, xp, yp, R2, _p(m))
+    return m
+
+
+# ---------------------------------------------------------------- O3
+def classify(scene):
+    """Class grid (uint8 H x W: 0 free, 1 obstacle, 2 goal) plus per-track t, j, (xp, yp, R2)."""
+    W, H = scene.W, scene.H
+    static = np.ascontiguousarray(scene.static, np.uint8)
+    tracks = np.ascontiguousarray(scene.tracks, np.float64).reshape(-1, 20)
+    n = tracks.shape[0]
+    cls = np.zeros((H, W), np.uint8)
+    t = np.zeros(max(n, 1), np.int32)
+    j = np.zeros(max(n, 1), np.int32)
+    pred = np.zeros((max(n, 1), 3))
+    wc = scene.warp
+    Q = np.ascontiguousarray(wc.Q, np.float64).reshape(16)
+    xr, yr, th, sp = scene.robot
+    st = lib().orc_classify(W, H, scene.cell_size, scene.origin[0], scene.origin[1], _p(static),
+                            int(scene.goal[0]), int(scene.goal[1]), xr, yr, th, sp,
+                            n, _p(tracks), wc.dt, _p(Q), wc.warp_spacing, wc.eps_v,
+                            wc.safety_radius, int(wc.horizon_max), _p(cls), _p(t), _p(j), _p(pred))
+    return st, cls, t[:n], j[:n], pred[:n]
+
+
+def robot_cell(scene):
+    xr, yr = scene.robot[0], scene.robot[1]
+    return (int(math.floor((xr - scene.origin[0]) / scene.cell_size)),
+            int(math.floor((yr - scene.origin[1]) / scene.cell_size)))
+
+
+def init_u32(cls, cls_prev=None, u_prev=None):
+    cls = np.ascontiguousarray(cls, np.uint8)
+    u = np.zeros(cls.shape, np.float32)
+    if cls_prev is None:
+        lib().orc_init_u32(cls.size, _p(cls), None, None, _p(u))
+    else:
+        cp = np.ascontiguousarray(cls_prev, np.uint8)
+        up = np.ascontiguousarray(u_prev, np.float32)
+        lib().orc_init_u32(cls.size, _p(cls), _p(cp), _p(up), _p(u))
+    return u
+
+
+def init_u64(cls):
+    cls = np.ascontiguousarray(cls, np.uint8)
+    u = np.zeros(cls.shape, np.float64)
+    lib().orc_init_u64(cls.size, _p(cls), _p(u))
+    return u
+
+
+# ---------------------------------------------------------------- O4, O5
+def relax_f32(cls, u, max_sweeps, check_every=1, tol=0.0):
+    """In-place red-black relaxation of float32 u.  Returns (sweeps, residual)."""
+    assert u.dtype == np.float32 and u.flags.c_contiguous
+    cls = np.ascontiguousarray(cls, np.uint8)
+    H, W = u.shape
+    r = np.zeros(1, np.float32)
+    s = lib().orc_relax_f32(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol), _p(r))
+    return int(s), float(r[0])
+
+
+def relax_f64(cls, u, max_sweeps, check_every=1, tol=0.0):
+    assert u.dtype == np.float64 and u.flags.c_contiguous
+    cls = np.ascontiguousarray(cls, np.uint8)
+    H, W = u.shape
+    r = np.zeros(1, np.float64)
+    s = lib().orc_relax_f64(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol), _p(r))
+    return int(s), float(r[0])
+
+
+def jacobi_f64(cls, u, max_sweeps, tol=0.0):
+    assert u.dtype == np.float64 and u.flags.c_contiguous
+    cls = np.ascontiguousarray(cls, np.uint8)
+    H, W = u.shape
+    r = np.zeros(1, np.float64)
+    s = lib().orc_jacobi_f64(W, H, _p(cls), _p(u), int(max_sweeps), float(tol), _p(r))
+    return int(s), float(r[0])
+
+
+# ---------------------------------------------------------------- O6-O8
+def walk(cls, u, start, max_len):
+    cls = np.ascontiguousarray(cls, np.uint8)
+    u = np.ascontiguousarray(u, np.float32)
+    H, W = u.shape
+    cells = np.zeros((max(max_len, 1), 2), np.int32)
+    n = np.zeros(1, np.int32)
+    st = lib().orc_walk(W, H, _p(cls), _p(u), int(start[0]), int(start[1]), int(max_len), _p(cells), _p(n))
+    return st, cells[: int(n[0])].copy()
+
+
+def bilerp(u, px, py):
+    u = np.ascontiguousarray(u, np.float32)
+    H, W = u.shape
+    return lib().orc_bilerp(W, H, _p(u), float(px), float(py))
+
+
+def band(cls, u, waypoints, iters=50, step=0.25, kt=1.0, sequential=False):
+    cls = np.ascontiguousarray(cls, np.uint8)
+    u = np.ascontiguousarray(u, np.float32)
+    H, W = u.shape
+    w = np.ascontiguousarray(waypoints, np.float32).reshape(-1, 2).copy()
+    f = lib().orc_band_sequential if sequential else lib().orc_band
+    f(W, H, _p(cls), _p(u), w.shape[0], _p(w), int(iters), np.float32(step), np.float32(kt))
+    return w
+
+
+def cells_to_waypoints(cells):
+    return (np.asarray(cells, np.float32).reshape(-1, 2) + np.float32(0.5)).astype(np.float32)
+
+
+def resample(w, max_out=None):
+    w = np.ascontiguousarray(w, np.float32).reshape(-1, 2)
+    cnt = lib().orc_resample(w.shape[0], _p(w), 0, None) if max_out is None else None
+    m = cnt if max_out is None else max_out
+    out = np.zeros((max(m, 1), 2), np.float32)
+    cnt = lib().orc_resample(w.shape[0], _p(w), m, _p(out))
+    return out[: min(cnt, m)].copy(), int(cnt)
+
+
+def next_waypoint(pts):
+    pts = np.ascontiguousarray(pts, np.float32).reshape(-1, 2)
+    nx = np.zeros(1, np.float32)
+    ny = np.zeros(1, np.float32)
+    k = lib().orc_next_waypoint(pts.shape[0], _p(pts), _p(nx), _p(ny))
+    return k, float(nx[0]), float(ny[0])
+
+
+def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0.25, kt=1.0,
+              max_len=None, prev=None):
+    """One planning tick, Algorithm 1 on the CPU.
+
+    prev: None (cold start) or the dict returned by the previous call (warm
+    start, C7).  Returns a dict with class grid, field (float32 u), sweeps,
+    residual, walk status/cells, smoothed path and next waypoint.
+    """
+    st, cls, t, j, pred = classify(scene)
+    if st < 0:
+        return {"status": st}
+    if prev is None:
+        u = init_u32(cls)
+    else:
+        u = init_u32(cls, prev["cls"], prev["u"])
+    sweeps, res = relax_f32(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol)
+    if max_len is None:
+        max_len = 4 * (scene.W + scene.H)
+    wst, cells = walk(cls, u, robot_cell(scene), max_len)
+    out = {"status": st, "cls": cls, "u": u, "t": t, "j": j, "pred": pred, "sweeps": sweeps,
+           "residual": res, "walk_status": wst, "cells": cells}
+    if wst == OK:
+        w = band(cls, u, cells_to_waypoints(cells), iters, step, kt)
+        sm, _ = resample(w)
+        k, nx, ny = next_waypoint(sm)
+        out.update(band=w, smooth=sm, next=(nx, ny))
+    else:
+        out.update(band=np.zeros((0, 2), np.float32), smooth=np.zeros((0, 2), np.float32), next=None)
+    return out

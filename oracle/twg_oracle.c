@@ -1,0 +1,547 @@
+/*
+ * twg_oracle.c -- plain, slow CPU oracle of the Time-Warped Grid hot path
+ * (arXiv 1903.07441).  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_1903_07441_b200/) never includes, links or calls it, and this file
+ * shares no code, header, table or constant generator with the CUDA path.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n, "S:n" = SPEC.md line n,
+ * "C<k>" = the reading recorded in DESIGN.md "Readings of the paper".
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared (no FMA
+ * contraction, no FTZ/DAZ), so every float/double expression below is the
+ * IEEE operation sequence written in the source, evaluated left to right.
+ *
+ * Representation: the oracle keeps its own uint8 class grid
+ * (ORC_FREE / ORC_OBSTACLE / ORC_GOAL) and stores the field as
+ * u = 1 - phi (C3), so goal u = 1, obstacle u = 0, free init 0.5.
+ *
+ * Parity-pinned functions: see the header of each function; the pins live in
+ * tests/test_oracle_pins.py.  Parity unpinned (defined only by the algorithm
+ * as written here): the exact smoothed path on general scenes (orc_band, only
+ * its properties are pinned), the warm-start trajectory over many ticks
+ * (orc_init_u32 warm branch), and the next-waypoint choice (orc_next_waypoint).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { ORC_FREE = 0, ORC_OBSTACLE = 1, ORC_GOAL = 2 };
+enum { ORC_OK = 0, ORC_W_GOAL_SWALLOWED = 1, ORC_E_INVALID_ARG = -1, ORC_E_OUT_OF_BOUNDS = -2,
+       ORC_E_OVERLAPPING = -3, ORC_E_INVALID_START = -4, ORC_E_NO_PATH = -5 };
+
+/* ------------------------------------------------------------------------ */
+/* O1  time-warp radius and warp number  (Eqs. 14-15; C16, C17)  */
+/* ------------------------------------------------------------------------ */
+
+/* Left-hand side of Eq. 14 for a given r_x, with the centre of
+ * P:463-465 (x_c = x_r + 0.9 r_x cos(theta)) and r_y = r_x / 4.
+ * Used by the pins to check the closed form below against the paper's
+ * implicit definition. */
+double orc_eq14_lhs(double xr, double yr, double c, double s, double xo, double yo, double rx)
+{
+    double xc = xr + 0.9 * rx * c;
+    double yc = yr + 0.9 * rx * s;
+    double ry = rx / 4.0;
+    double A = c * (xo - xc) + s * (yo - yc);
+    double B = s * (xo - xc) - c * (yo - yc);
+    return (A * A) / (rx * rx) + (B * B) / (ry * ry);
+}
+
+/* Eq. 15 is implicit because (x_c, y_c) depend on r_x.
+ * With a = c dx + s dy, b = s dx - c dy (dx = x_obj - x_r): the rotated
+ * offsets from the centre are a - 0.9 r and b, so Eq. 15 squared reads
+ *   r^2 = (a - 0.9 r)^2 + 16 b^2  <=>  0.19 r^2 + 1.8 a r - (a^2 + 16 b^2) = 0,
+ * whose unique non-negative root is (C16)
+ *   r = (sqrt(4 a^2 + 12.16 b^2) - 1.8 a) / 0.38.                          */
+double orc_warp_radius(double xr, double yr, double c, double s, double xo, double yo)
+{
+    double dx = xo - xr;
+    double dy = yo - yr;
+    double a = c * dx + s * dy;
+    double b = s * dx - c * dy;
+    return (sqrt(4.0 * a * a + 12.16 * b * b) - 1.8 * a) / 0.38;
+}
+
+/* Warp number t = max(1, ceil(r_x / w)) ("label the obstacle with
+ * the corresponding warp number"; C17). */
+int32_t orc_warp_number(double rx, double w)
+{
+    double t = ceil(rx / w);
+    if (t < 1.0) t = 1.0;
+    return (int32_t)t;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O2  horizon j and j-step Kalman predict  (Eqs. 9-10, 16-17)   */
+/* ------------------------------------------------------------------------ */
+
+/* Eq. 16: Time-Warp = v t, v = ratio of robot speed to obstacle
+ * speed (C18): v = speed_r / max(|v_hat|, eps_v), j = clamp(round(v t), 0,
+ * horizon_max), round = half away from zero (llround, C25). */
+int32_t orc_horizon(int32_t t, double speed_r, double vx, double vy, double eps_v, int32_t hmax)
+{
+    double so = sqrt(vx * vx + vy * vy);
+    if (so < eps_v) so = eps_v;
+    double v = speed_r / so;
+    long long j = llround(v * (double)t);
+    if (j < 0) j = 0;
+    if (j > hmax) j = hmax;
+    return (int32_t)j;
+}
+
+/* A of P:548-553: constant velocity, dt in the (0,2) and (1,3) slots. */
+static void orc_A(double dt, double A[16])
+{
+    memset(A, 0, 16 * sizeof(double));
+    A[0] = 1.0; A[5] = 1.0; A[10] = 1.0; A[15] = 1.0;
+    A[0 * 4 + 2] = dt;
+    A[1 * 4 + 3] = dt;
+}
+
+/* j applications of Eq. 9 (x <- A x) and Eq. 10 (P <- A P A^T + Q,
+ * P:376), B = 0.  Dense 4x4 products, k ascending, separate * and +. */
+void orc_predict(const double* x, const double* P, const double* Q, double dt, int32_t j,
+                 double* xo, double* Po)
+{
+    double A[16], xc[4], Pc[16], AP[16], xn[4];
+    orc_A(dt, A);
+    memcpy(xc, x, sizeof xc);
+    memcpy(Pc, P, sizeof Pc);
+    for (int32_t step = 0; step < j; ++step) {
+        for (int r = 0; r < 4; ++r) {
+            double acc = 0.0;
+            for (int k = 0; k < 4; ++k) acc = acc + A[r * 4 + k] * xc[k];
+            xn[r] = acc;
+        }
+        memcpy(xc, xn, sizeof xc);
+        for (int r = 0; r < 4; ++r)
+            for (int col = 0; col < 4; ++col) {
+                double acc = 0.0;
+                for (int k = 0; k < 4; ++k) acc = acc + A[r * 4 + k] * Pc[k * 4 + col];
+                AP[r * 4 + col] = acc;
+            }
+        for (int r = 0; r < 4; ++r)
+            for (int col = 0; col < 4; ++col) {
+                double acc = 0.0;
+                for (int k = 0; k < 4; ++k) acc = acc + AP[r * 4 + k] * A[col * 4 + k];
+                Pc[r * 4 + col] = acc + Q[r * 4 + col];
+            }
+    }
+    memcpy(xo, xc, sizeof xc);
+    memcpy(Po, Pc, sizeof Pc);
+}
+
+/* Footprint radius^2 (P:492-505 Gaussian "based on the calculated
+ * uncertainty ... and a desired safety distance"; C19, C20):
+ * sigma^2 = (P00 + P11) / 2; exp(-d^2 / (2 sigma^2)) >= 1/2  <=>
+ * d^2 <= 2 ln 2 sigma^2; union with the safety disk d <= r_s. */
+double orc_footprint_r2(const double* P, double rs)
+{
+    double sig2 = (P[0] + P[5]) * 0.5;
+    double g = 1.3862943611198906 * sig2; /* 2 ln 2 */
+    double s2 = rs * rs;
+    return g > s2 ? g : s2;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O3  class grid: static walls, time-warped stamps, goal, robot exemption  */
+/* (Alg. 1; C20-C22)                        */
+/* ------------------------------------------------------------------------ */
+
+/* tracks: n x 20 doubles (x[4], P[16] row-major).  Outputs the class grid
+ * (row-major H x W), and per track t, j and (x_pred, y_pred, R^2).
+ * Membership of cell (i, k): (ox + (i + 0.5) cs - xp)^2 + (oy + (k + 0.5) cs
+ * - yp)^2 <= R^2 in double.  The loop box is a superset of the disk (pin P4
+ * checks it against the all-cells loop, orc_stamp_bruteforce). */
+static void orc_stamp_one(int32_t W, int32_t H, double cs, double ox, double oy,
+                          double xp, double yp, double R2, uint8_t* stamp, int32_t box)
+{
+    int32_t i0 = 0, i1 = W - 1, k0 = 0, k1 = H - 1;
+    if (box) {
+        double R = sqrt(R2);
+        double lo_x = floor((xp - R - ox) / cs) - 2.0, hi_x = ceil((xp + R - ox) / cs) + 2.0;
+        double lo_y = floor((yp - R - oy) / cs) - 2.0, hi_y = ceil((yp + R - oy) / cs) + 2.0;
+        if (hi_x < 0.0 || hi_y < 0.0 || lo_x > (double)(W - 1) || lo_y > (double)(H - 1)) return;
+        if (lo_x > i0) i0 = (int32_t)lo_x;
+        if (hi_x < i1) i1 = (int32_t)hi_x;
+        if (lo_y > k0) k0 = (int32_t)lo_y;
+        if (hi_y < k1) k1 = (int32_t)hi_y;
+    }
+    for (int32_t k = k0; k <= k1; ++k)
+        for (int32_t i = i0; i <= i1; ++i) {
+            double cx = ox + ((double)i + 0.5) * cs;
+            double cy = oy + ((double)k + 0.5) * cs;
+            double dx = cx - xp;
+            double dy = cy - yp;
+            if (dx * dx + dy * dy <= R2) stamp[(size_t)k * W + i] = 1;
+        }
+}
+
+/* Stamp a single disk with the all-cells loop (pin P4 only). */
+void orc_stamp_bruteforce(int32_t W, int32_t H, double cs, double ox, double oy,
+                          double xp, double yp, double R2, uint8_t* stamp)
+{
+    orc_stamp_one(W, H, cs, ox, oy, xp, yp, R2, stamp, 0);
+}
+
+void orc_stamp_box(int32_t W, int32_t H, double cs, double ox, double oy,
+                   double xp, double yp, double R2, uint8_t* stamp)
+{
+    orc_stamp_one(W, H, cs, ox, oy, xp, yp, R2, stamp, 1);
+}
+
+int32_t orc_classify(int32_t W, int32_t H, double cs, double ox, double oy,
+                     const uint8_t* static_mask, int32_t gx, int32_t gy,
+                     double xr, double yr, double theta, double speed,
+                     int32_t n, const double* tracks,
+                     double dt, const double* Q, double w, double eps_v, double rs, int32_t hmax,
+                     uint8_t* cls, int32_t* t_out, int32_t* j_out, double* pred_out)
+{
+    if (W <= 0 || H <= 0 || cs <= 0.0 || n < 0) return ORC_E_INVALID_ARG;
+    /* goal in bounds and not on a static wall */
+    if (gx < 0 || gy < 0 || gx >= W || gy >= H) return ORC_E_OUT_OF_BOUNDS;
+    if (static_mask[(size_t)gy * W + gx]) return ORC_E_OVERLAPPING;
+    /* robot cell = floor((x_r - o_x) / cs) (S:41 floor binning) */
+    double fxr = floor((xr - ox) / cs), fyr = floor((yr - oy) / cs);
+    if (fxr < 0.0 || fyr < 0.0 || fxr >= (double)W || fyr >= (double)H) return ORC_E_OUT_OF_BOUNDS;
+    int32_t rcx = (int32_t)fxr, rcy = (int32_t)fyr;
+    if (static_mask[(size_t)rcy * W + rcx]) return ORC_E_INVALID_START;
+
+    size_t ncell = (size_t)W * H;
+    uint8_t* stamp = (uint8_t*)calloc(ncell, 1);
+    if (!stamp) return ORC_E_INVALID_ARG;
+    double c = cos(theta), s = sin(theta);
+    for (int32_t i = 0; i < n; ++i) {
+        const double* x = tracks + (size_t)i * 20;
+        const double* P = x + 4;
+        double rx = orc_warp_radius(xr, yr, c, s, x[0], x[1]);      /* O1, C24: from x_hat */
+        int32_t t = orc_warp_number(rx, w);
+        int32_t j = orc_horizon(t, speed, x[2], x[3], eps_v, hmax);  /* O2 */
+        double xo[4], Po[16];
+        orc_predict(x, P, Q, dt, j, xo, Po);
+        double R2 = orc_footprint_r2(Po, rs);
+        if (t_out) t_out[i] = t;
+        if (j_out) j_out[i] = j;
+        if (pred_out) { pred_out[3 * i] = xo[0]; pred_out[3 * i + 1] = xo[1]; pred_out[3 * i + 2] = R2; }
+        orc_stamp_one(W, H, cs, ox, oy, xo[0], xo[1], R2, stamp, 1);
+    }
+    int32_t status = ORC_OK;
+    if (stamp[(size_t)gy * W + gx]) status = ORC_W_GOAL_SWALLOWED;
+    /* precedence (C22): goal > robot-cell exemption > (static U stamped) > free */
+    for (size_t q = 0; q < ncell; ++q)
+        cls[q] = (static_mask[q] || stamp[q]) ? ORC_OBSTACLE : ORC_FREE;
+    cls[(size_t)rcy * W + rcx] = ORC_FREE;
+    cls[(size_t)gy * W + gx] = ORC_GOAL;
+    free(stamp);
+    return status;
+}
+
+/* Field initialisation in u-space (C7).
+ * cold (cls_prev == NULL): goal 1, obstacle 0, free 0.5 ("initialized with 0.5").
+ * warm: fixed-now cells take their fixed value; cells fixed in the previous
+ * tick and free now restart at 0.5; other free cells keep u_prev
+ * ("the values evolve slowly anyways"). */
+void orc_init_u32(int64_t ncell, const uint8_t* cls, const uint8_t* cls_prev,
+                  const float* u_prev, float* u)
+{
+    for (int64_t q = 0; q < ncell; ++q) {
+        if (cls[q] == ORC_GOAL) u[q] = 1.0f;
+        else if (cls[q] == ORC_OBSTACLE) u[q] = 0.0f;
+        else if (cls_prev == NULL || cls_prev[q] != ORC_FREE) u[q] = 0.5f;
+        else u[q] = u_prev[q];
+    }
+}
+
+void orc_init_u64(int64_t ncell, const uint8_t* cls, double* u)
+{
+    for (int64_t q = 0; q < ncell; ++q)
+        u[q] = cls[q] == ORC_GOAL ? 1.0 : (cls[q] == ORC_OBSTACLE ? 0.0 : 0.5);
+}
+
+/* ------------------------------------------------------------------------ */
+/* O4-O5  red-black Gauss-Seidel relaxation + stop rule                     */
+/* (Eqs. 1-2, Alg. 1; C1, C2, C4-C6)  */
+/* ------------------------------------------------------------------------ */
+
+/* Cells with cls != ORC_FREE are fixed (Dirichlet) and keep the value they
+ * hold in u, so tests may pass general fixed values (pin P8).  Outside the
+ * grid u = 0 (C4: outside = obstacle).  One sweep = red pass ((x+y) even, in
+ * the grid's own coordinates) then black pass; each free cell becomes
+ * 0.25 * ((E + W) + (N + S)) (C2).  res_s = max |new - old| over the free
+ * cells of sweep s.  Stop after sweep s when (s % check_every == 0 and
+ * res_s < tol) or s == max_sweeps.  Returns sweeps done; *res_out = res_s of
+ * the last sweep (0 if none). */
+int32_t orc_relax_f32(int32_t W, int32_t H, const uint8_t* cls, float* u,
+                      int32_t max_sweeps, int32_t check_every, float tol, float* res_out)
+{
+    float res = 0.0f;
+    int32_t s = 0;
+    if (check_every < 1) check_every = 1;
+    for (s = 1; s <= max_sweeps; ++s) {
+        res = 0.0f;
+        for (int color = 0; color < 2; ++color)
+            for (int32_t y = 0; y < H; ++y)
+                for (int32_t x = 0; x < W; ++x) {
+                    if (((x + y) & 1) != color) continue;
+                    size_t q = (size_t)y * W + x;
+                    if (cls[q] != ORC_FREE) continue;
+                    float uE = x + 1 < W ? u[q + 1] : 0.0f;
+                    float uW = x > 0 ? u[q - 1] : 0.0f;
+                    float uN = y > 0 ? u[q - W] : 0.0f;
+                    float uS = y + 1 < H ? u[q + W] : 0.0f;
+                    float nv = 0.25f * ((uE + uW) + (uN + uS));
+                    float d = fabsf(nv - u[q]);
+                    if (d > res) res = d;
+                    u[q] = nv;
+                }
+        if ((s % check_every == 0 && res < tol) || s == max_sweeps) break;
+    }
+    if (max_sweeps <= 0) { s = 0; res = 0.0f; }
+    if (res_out) *res_out = res;
+    return s;
+}
+
+int32_t orc_relax_f64(int32_t W, int32_t H, const uint8_t* cls, double* u,
+                      int32_t max_sweeps, int32_t check_every, double tol, double* res_out)
+{
+    double res = 0.0;
+    int32_t s = 0;
+    if (check_every < 1) check_every = 1;
+    for (s = 1; s <= max_sweeps; ++s) {
+        res = 0.0;
+        for (int color = 0; color < 2; ++color)
+            for (int32_t y = 0; y < H; ++y)
+                for (int32_t x = 0; x < W; ++x) {
+                    if (((x + y) & 1) != color) continue;
+                    size_t q = (size_t)y * W + x;
+                    if (cls[q] != ORC_FREE) continue;
+                    double uE = x + 1 < W ? u[q + 1] : 0.0;
+                    double uW = x > 0 ? u[q - 1] : 0.0;
+                    double uN = y > 0 ? u[q - W] : 0.0;
+                    double uS = y + 1 < H ? u[q + W] : 0.0;
+                    double nv = 0.25 * ((uE + uW) + (uN + uS));
+                    double d = fabs(nv - u[q]);
+                    if (d > res) res = d;
+                    u[q] = nv;
+                }
+        if ((s % check_every == 0 && res < tol) || s == max_sweeps) break;
+    }
+    if (max_sweeps <= 0) { s = 0; res = 0.0; }
+    if (res_out) *res_out = res;
+    return s;
+}
+
+/* Jacobi, Eq. 1 literally: every free cell from the previous
+ * iterate.  Oracle-only variant for pins P7 and P12 (Jacobi and red-black
+ * share the fixed point). */
+int32_t orc_jacobi_f64(int32_t W, int32_t H, const uint8_t* cls, double* u,
+                       int32_t max_sweeps, double tol, double* res_out)
+{
+    size_t ncell = (size_t)W * H;
+    double* old = (double*)malloc(ncell * sizeof(double));
+    double res = 0.0;
+    int32_t s = 0;
+    for (s = 1; s <= max_sweeps; ++s) {
+        memcpy(old, u, ncell * sizeof(double));
+        res = 0.0;
+        for (int32_t y = 0; y < H; ++y)
+            for (int32_t x = 0; x < W; ++x) {
+                size_t q = (size_t)y * W + x;
+                if (cls[q] != ORC_FREE) continue;
+                double uE = x + 1 < W ? old[q + 1] : 0.0;
+                double uW = x > 0 ? old[q - 1] : 0.0;
+                double uN = y > 0 ? old[q - W] : 0.0;
+                double uS = y + 1 < H ? old[q + W] : 0.0;
+                double nv = 0.25 * ((uE + uW) + (uN + uS));
+                double d = fabs(nv - old[q]);
+                if (d > res) res = d;
+                u[q] = nv;
+            }
+        if (res < tol || s == max_sweeps) break;
+    }
+    if (max_sweeps <= 0) { s = 0; res = 0.0; }
+    free(old);
+    if (res_out) *res_out = res;
+    return s;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O6  descent walk on the implicit index matrix                            */
+/* (Eq. 3, Alg. 1; C8, C9)   */
+/* ------------------------------------------------------------------------ */
+
+/* Eq. 3's argmin of phi is the argmax of u = 1 - phi.  From the robot cell:
+ *   if c is the goal: done; if c is an obstacle: NoPath;
+ *   n = in-bounds 4-neighbour with the largest u, scanned [+x, -x, +y, -y],
+ *       replaced only on strictly greater (first maximum wins);
+ *   append n; if the path is longer than max_len: NoPath.
+ * On NoPath *n_cells = 0.  cells_xy holds max_len (x, y) pairs. */
+int32_t orc_walk(int32_t W, int32_t H, const uint8_t* cls, const float* u,
+                 int32_t sx, int32_t sy, int32_t max_len, int32_t* cells_xy, int32_t* n_cells)
+{
+    static const int dxs[4] = { +1, -1, 0, 0 };
+    static const int dys[4] = { 0, 0, +1, -1 };
+    int32_t n = 0, x = sx, y = sy;
+    *n_cells = 0;
+    if (max_len < 1) return ORC_E_NO_PATH;
+    cells_xy[0] = x; cells_xy[1] = y; n = 1;
+    for (;;) {
+        uint8_t k = cls[(size_t)y * W + x];
+        if (k == ORC_GOAL) { *n_cells = n; return ORC_OK; }
+        if (k == ORC_OBSTACLE) return ORC_E_NO_PATH;
+        int bx = -1, by = -1;
+        float best = 0.0f;
+        int have = 0;
+        for (int d = 0; d < 4; ++d) {
+            int nx = x + dxs[d], ny = y + dys[d];
+            if (nx < 0 || ny < 0 || nx >= W || ny >= H) continue;
+            float v = u[(size_t)ny * W + nx];
+            if (!have || v > best) { best = v; bx = nx; by = ny; have = 1; }
+        }
+        if (!have) return ORC_E_NO_PATH; /* 1x1 grid with a free cell */
+        if (n + 1 > max_len) return ORC_E_NO_PATH;
+        x = bx; y = by;
+        cells_xy[2 * n] = x; cells_xy[2 * n + 1] = y; ++n;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O7  rubber band (Eqs. 4-6, Fig. 1)        */
+/* ------------------------------------------------------------------------ */
+
+/* u at a continuous position (cell units) by bilinear interpolation of the
+ * cell-centred samples at (i + 0.5, k + 0.5); samples outside the grid are 0
+ * (C4, C14).  Evaluated as (1-ty)((1-tx)u00 + tx u10) + ty((1-tx)u01 + tx u11). */
+static float orc_u_at(int32_t W, int32_t H, const float* u, int32_t i, int32_t k)
+{
+    if (i < 0 || k < 0 || i >= W || k >= H) return 0.0f;
+    return u[(size_t)k * W + i];
+}
+
+float orc_bilerp(int32_t W, int32_t H, const float* u, float px, float py)
+{
+    float fx = px - 0.5f, fy = py - 0.5f;
+    float x0f = floorf(fx), y0f = floorf(fy);
+    float tx = fx - x0f, ty = fy - y0f;
+    int32_t x0 = (int32_t)x0f, y0 = (int32_t)y0f;
+    float u00 = orc_u_at(W, H, u, x0, y0);
+    float u10 = orc_u_at(W, H, u, x0 + 1, y0);
+    float u01 = orc_u_at(W, H, u, x0, y0 + 1);
+    float u11 = orc_u_at(W, H, u, x0 + 1, y0 + 1);
+    float a = (1.0f - tx) * u00 + tx * u10;
+    float b = (1.0f - tx) * u01 + tx * u11;
+    return (1.0f - ty) * a + ty * b;
+}
+
+/* One waypoint update (Eq. 4 argmin over the current position and 8 offsets
+ * of length `step` (C12); Eq. 5 moves the waypoint there).
+ * Tensions T = k_t (w_{i+-1} - c) (C11).  Eq. 6 in u-space:
+ * F = 1/u(c) - 1/u(w_i) (P:311-313 with 1 - phi = u), acting along the
+ * candidate direction d_hat with F_vec = -F d_hat (C13); candidates whose
+ * cell is off-grid or an obstacle, or with u <= 1e-9, are skipped (S:208,
+ * S:216-217).  The current position (F_vec = 0) wins all ties. */
+static void orc_band_point(int32_t W, int32_t H, const uint8_t* cls, const float* u,
+                           const float* wp, const float* wi, const float* wn,
+                           float step, float kt, float* out)
+{
+    static const float ox[8] = { +1.f, -1.f, 0.f, 0.f, +1.f, +1.f, -1.f, -1.f };
+    static const float oy[8] = { 0.f, 0.f, +1.f, -1.f, +1.f, -1.f, +1.f, -1.f };
+    float bx = wi[0], by = wi[1];
+    float tx = kt * (wp[0] - wi[0]) + kt * (wn[0] - wi[0]);
+    float ty = kt * (wp[1] - wi[1]) + kt * (wn[1] - wi[1]);
+    float best = tx * tx + ty * ty;
+    float uw = orc_bilerp(W, H, u, wi[0], wi[1]);
+    for (int d = 0; d < 8; ++d) {
+        float cx = wi[0] + step * ox[d];
+        float cy = wi[1] + step * oy[d];
+        float fcx = floorf(cx), fcy = floorf(cy);
+        if (fcx < 0.0f || fcy < 0.0f || fcx >= (float)W || fcy >= (float)H) continue;
+        if (cls[(size_t)(int32_t)fcy * W + (int32_t)fcx] == ORC_OBSTACLE) continue;
+        float uc = orc_bilerp(W, H, u, cx, cy);
+        if (uc <= 1e-9f || uw <= 1e-9f) continue;
+        float F = 1.0f / uc - 1.0f / uw;
+        float hx = d < 4 ? ox[d] : ox[d] * 0.70710678f;
+        float hy = d < 4 ? oy[d] : oy[d] * 0.70710678f;
+        float Rx = (-(F * hx) + kt * (wp[0] - cx)) + kt * (wn[0] - cx);
+        float Ry = (-(F * hy) + kt * (wp[1] - cy)) + kt * (wn[1] - cy);
+        float r2 = Rx * Rx + Ry * Ry;
+        if (r2 < best) { best = r2; bx = cx; by = cy; }
+    }
+    out[0] = bx; out[1] = by;
+}
+
+/* I iterations; each iteration updates the odd interior waypoints, then the
+ * even ones (C10: parity order; the two waypoints each one reads are of the
+ * other parity, so in-place update equals "reads before the phase").
+ * Endpoints never move. w: n (x, y) pairs in cell units, in/out. */
+void orc_band(int32_t W, int32_t H, const uint8_t* cls, const float* u,
+              int32_t n, float* w, int32_t iters, float step, float kt)
+{
+    for (int32_t it = 0; it < iters; ++it)
+        for (int p = 1; p >= 0; --p)
+            for (int32_t i = 1; i + 1 < n; ++i) {
+                if ((i & 1) != p) continue;
+                float o[2];
+                orc_band_point(W, H, cls, u, w + 2 * (i - 1), w + 2 * i, w + 2 * (i + 1), step, kt, o);
+                w[2 * i] = o[0]; w[2 * i + 1] = o[1];
+            }
+}
+
+/* SPEC.md:235's literal sequential order (start to goal), oracle-only, used
+ * by property tests of the band (not a parity target). */
+void orc_band_sequential(int32_t W, int32_t H, const uint8_t* cls, const float* u,
+                         int32_t n, float* w, int32_t iters, float step, float kt)
+{
+    for (int32_t it = 0; it < iters; ++it)
+        for (int32_t i = 1; i + 1 < n; ++i) {
+            float o[2];
+            orc_band_point(W, H, cls, u, w + 2 * (i - 1), w + 2 * i, w + 2 * (i + 1), step, kt, o);
+            w[2 * i] = o[0]; w[2 * i + 1] = o[1];
+        }
+}
+
+/* Resample (C15): each segment of length l is replaced by
+ * ceil(max(l, 1)) equal sub-steps p = w_i + (k / m) (w_{i+1} - w_i); the
+ * last waypoint is appended.  Returns the number of points (only the first
+ * max_out are written). */
+int32_t orc_resample(int32_t n, const float* w, int32_t max_out, float* out)
+{
+    int32_t cnt = 0;
+    if (n <= 0) return 0;
+    for (int32_t i = 0; i + 1 < n; ++i) {
+        float dx = w[2 * (i + 1)] - w[2 * i];
+        float dy = w[2 * (i + 1) + 1] - w[2 * i + 1];
+        float l = sqrtf(dx * dx + dy * dy);
+        int32_t m = (int32_t)ceilf(l > 1.0f ? l : 1.0f);
+        for (int32_t k = 0; k < m; ++k) {
+            float t = (float)k / (float)m;
+            if (cnt < max_out) {
+                out[2 * cnt] = w[2 * i] + t * dx;
+                out[2 * cnt + 1] = w[2 * i + 1] + t * dy;
+            }
+            ++cnt;
+        }
+    }
+    if (cnt < max_out) { out[2 * cnt] = w[2 * (n - 1)]; out[2 * cnt + 1] = w[2 * (n - 1) + 1]; }
+    ++cnt;
+    return cnt;
+}
+
+/* O8 (Alg. 1 P:705-706 "Move the robot to the next cell on the current path";
+ * S:233): the first resampled waypoint at distance >= 1 cell from the first
+ * one (the robot's cell centre), else the last (the goal). */
+int32_t orc_next_waypoint(int32_t n, const float* pts, float* nx, float* ny)
+{
+    if (n <= 0) return -1;
+    for (int32_t i = 1; i < n; ++i) {
+        float dx = pts[2 * i] - pts[0];
+        float dy = pts[2 * i + 1] - pts[1];
+        if (dx * dx + dy * dy >= 1.0f) { *nx = pts[2 * i]; *ny = pts[2 * i + 1]; return i; }
+    }
+    *nx = pts[2 * (n - 1)]; *ny = pts[2 * (n - 1) + 1];
+    return n - 1;
+}
