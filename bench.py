@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""Benchmark of the Time-Warped Grid hot path on B200 (BASELINE.json metric:
+"harmonic relaxation GLUP/s and plan steps/sec at 4096^2; % of HBM roofline").
+
+A step = one planning tick of Algorithm 1 through the C ABI:
+twg_plan_step = rows a1-a3 (time-warped stamping of 200 Kalman tracks) + a4-a6
+(S = 100 red-black sweeps, warm start, Alg. 1) + a7-a9 (descent walk,
+50 rubber-band iterations, resampling, next waypoint), on config C3
+(4096 x 4096, 200 moving obstacles, BASELINE.json configs[2]).
+
+  value       = 4096^2 * S * K / (device time of K steps), inputs resident in HBM
+  e2e         = same metric, tracks copied from pinned host memory and the path
+                read back to the host inside every timed step
+  relax_glups = kernel-only relaxation throughput (twg_relax, S = 1000)
+  roofline    = k_rb_tblock (the dominant kernel): 8 B per cell per launch
+                (one fp32 read + one fp32 write; T sweeps fused on chip) over its
+                CUDA-event launch time, vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline= the oracle (oracle/, single thread) on a bounded sample
+
+N > 1 (torchrun): every rank plans its own independent 4096^2 scenario
+(seed = rank): the units shard with no data-path collective ("weak").
+--impl reference times the CPU oracle (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "harmonic relaxation GLUP/s and plan steps/sec at 4096^2; % of HBM roofline"
+UNIT = "GLUP/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sweeps", type=int, default=100)
+    ap.add_argument("--band-iters", type=int, default=50)
+    ap.add_argument("--relax-sweeps", type=int, default=1000)
+    ap.add_argument("--T", type=int, default=0, help="temporal depth (0 = library default)")
+    ap.add_argument("--rows", type=int, default=0, help="rows per warp (0 = library default)")
+    ap.add_argument("--size", type=int, default=4096)
+    ap.add_argument("--obstacles", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    return ap.parse_args()
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _scene(args, seed):
+    from scenes import scene_random
+    n_seg = max(1, int(512 * (args.size / 4096) ** 2))
+    return scene_random(f"c3_{args.size}_s{seed}", args.size, n_seg, args.obstacles, seed)
+
+
+class Clocks:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index, enabled=True):
+        self.index, self.enabled, self.proc = index, enabled, None
+
+    def __enter__(self):
+        if self.enabled:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                              "--format=csv,noheader,nounits", "-lms", "200"],
+                                             stdout=self.f, stderr=subprocess.DEVNULL)
+                time.sleep(0.3)
+            except OSError:
+                self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if self.proc is None:
+            return None
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        load = [v for v in sm if v > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- CPU oracle arm
+def _oracle_sample(args, sweeps, steps, seed=0):
+    """Oracle plan steps (single thread, as it stands) on the same workload; GLUP/s."""
+    import oracle
+    from scenes import advance_scene
+    sc0 = _scene(args, seed)
+    prev = None
+    t_total, lups = 0.0, 0
+    for k in range(steps):
+        sc = advance_scene(sc0, k)
+        t0 = time.perf_counter()
+        prev = oracle.plan_step(sc, max_sweeps=sweeps, iters=args.band_iters, max_len=4 * (sc.W + sc.H), prev=prev)
+        t_total += time.perf_counter() - t0
+        lups += sc.W * sc.H * sweeps
+    return lups / t_total / 1e9, t_total
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    s = max(1, min(args.sweeps, 25))
+    _oracle_sample(args, s, args.warmup)
+    g, t = _oracle_sample(args, s, args.steps)
+    line = {"metric": METRIC, "value": g, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"c3_{args.size}: {args.size}x{args.size} grid, {args.obstacles} moving obstacles, "
+                                   f"one plan step per step (oracle sample: S={s} sweeps, I={args.band_iters})",
+                       "sweeps": s},
+            "cpu_baseline": {"value": g, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} oracle plan steps of c3 seed 0 with S={s} sweeps"},
+            "e2e": {"value": g, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1903_07441_b200 import Planner, band_cfg, relax_cfg, warp_cfg, lib
+    from scenes import advance_scene
+    lib()
+    stream = torch.cuda.current_stream(dev)
+    sc0 = _scene(args, rank)
+    N = sc0.W
+    wc = warp_cfg()
+    bc = band_cfg(args.band_iters, 4 * (sc0.W + sc0.H), 8 * (sc0.W + sc0.H))
+    pl = Planner(sc0.W, sc0.H, 1, sc0.cell_size, sc0.origin, device=local, stream=stream.cuda_stream)
+    pl.set_static(sc0.static)
+    # tick 0: cold start then a converging warm-up so the timed field is a warm planning field
+    st, res, _, _ = pl.plan_step(0, [sc0.robot], [sc0.goal], sc0.tracks, [sc0.n_tracks], wc,
+                                 relax_cfg(max_sweeps=2000, warm_start=0, temporal_depth=args.T,
+                                           rows_per_warp=args.rows), bc, want_paths=False)
+    rc = relax_cfg(max_sweeps=args.sweeps, warm_start=1, temporal_depth=args.T, rows_per_warp=args.rows)
+    n_ticks = args.warmup + args.steps
+    scenes = [advance_scene(sc0, 1 + k) for k in range(n_ticks)]
+    dev_tracks = [torch.from_numpy(np.ascontiguousarray(s.tracks)).to(dev) for s in scenes]
+    pin_tracks = [torch.from_numpy(np.ascontiguousarray(s.tracks)).pin_memory() for s in scenes]
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+    cells_h = np.zeros((1, bc.max_len, 2), np.int32)
+
+    def one(k, host):
+        s = scenes[k]
+        t = pin_tracks[k] if host else dev_tracks[k]
+        return pl.plan_step(0, [s.robot], [s.goal], t, [s.n_tracks], wc, rc, bc, want_paths=host)
+
+    def timed_loop(host):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for k in range(args.warmup):
+            one(k, host)
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        l0 = pl.kernel_launches()
+        walk = []
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[k][0].record(stream)
+            _, r, _, _ = one(args.warmup + k, host)
+            ev[k][1].record(stream)
+            walk.append(r[0].walk_status)
+        torch.cuda.synchronize(dev)
+        launches = pl.kernel_launches() - l0
+        ms = sum(a.elapsed_time(b) for a, b in ev)
+        if ws > 1:
+            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.barrier()
+            ms = float(tt.item())
+        return ms, launches, walk
+
+    with Clocks(local, enabled=not args.no_clocks) as clk:
+        pl.profile(1)
+        ms, launches, walk = timed_loop(host=False)
+        rms, rl, rcells = pl.profile_read()
+        pl.profile(0)
+    clocks = clk.summary()
+    ms_e2e, _, _ = timed_loop(host=True)
+
+    # kernel-only relaxation throughput (S = relax_sweeps), same field
+    rc_big = relax_cfg(max_sweeps=args.relax_sweeps, warm_start=1, temporal_depth=args.T, rows_per_warp=args.rows)
+    pl.relax(rc_big, want_result=False)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.zero_()
+    e0.record(stream)
+    pl.relax(rc_big, want_result=False)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    relax_ms = e0.elapsed_time(e1)
+
+    cells = N * N
+    units = cells * args.sweeps * args.steps * ws
+    value = units / (ms * 1e-3) / 1e9
+    e2e = units / (ms_e2e * 1e-3) / 1e9
+    peak, peak_src = _peaks()
+    avg_launch_s = (rms / rl) * 1e-3 if rl else float("nan")
+    T_eff = rcells / rl / cells if rl else 0
+    bytes_per_launch = 8.0 * cells  # one fp32 read + one fp32 write per cell per launch
+    achieved = bytes_per_launch / avg_launch_s / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"c3_{N}: {N}x{N} grid, {sc0.n_tracks} moving obstacles (Kalman tracks), warm "
+                               f"plan step = stamp + {args.sweeps} red-black sweeps + walk + {args.band_iters} "
+                               f"rubber-band iterations", "sweeps": args.sweeps, "band_iters": args.band_iters,
+                   "temporal_depth": args.T or 4, "l2": "flushed (256 MiB write) between timed steps",
+                   "per_rank": "independent scenario (seed = rank)"},
+        "plan_steps_per_s": args.steps * ws / (ms * 1e-3),
+        "relax_glups": cells * args.relax_sweeps / (relax_ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "k_rb_tblock", "bytes_per_launch": bytes_per_launch,
+                     "sweeps_per_launch": T_eff, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,
+                     "effective_glups_vs_8B_per_LUP": (rcells / (rms * 1e-3) / 1e9) / (peak / 8.0) if rms else None},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(sc0.n_tracks * 160 + 40),
+                "d2h_bytes_per_step": int(bc.max_len * 8 + bc.max_smooth * 8 + 32), "ms_per_step": ms_e2e / args.steps},
+        "gpu_launches": int(launches),
+        "walk_ok_steps": int(sum(1 for w in walk if w == 0)),
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        g, t = _oracle_sample(args, args.sweeps, 2)
+        out["cpu_baseline"] = {"value": g, "unit": UNIT, "cores": 1, "kind": "oracle",
+                               "sample": f"2 warm oracle plan steps of c3 seed 0 (S={args.sweeps}, "
+                                         f"I={args.band_iters}), {t:.1f} s, single thread"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    pl.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

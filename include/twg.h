@@ -1,0 +1,246 @@
+/*
+ * twg.h -- C ABI of the B200-native Time-Warped Grid hot path
+ * (arXiv 1903.07441, "Dynamic Path Planning via Time-Warped Grids").
+ *
+ * The library (libtwg.so, built from paper_1903_07441_b200/csrc/) runs every
+ * step of the planner's data-parallel hot path in hand-written sm_100a CUDA
+ * kernels:
+ *   a1-a3  time-warped obstacle rasterisation   twg_set_obstacles
+ *   a4-a6  red-black Laplace relaxation + residual + convergence control
+ *                                                twg_relax
+ *   a7-a9  descent walk + rubber band + next waypoint
+ *                                                twg_extract_path
+ *   all    one planning tick (Algorithm 1)       twg_plan_step
+ *
+ * Citations: "P:n" = PAPER.md line n (Eq./Alg. named), "S:n" = SPEC.md line n,
+ * "C<k>" = the reading recorded in DESIGN.md "Readings of the paper".
+ *
+ * Conventions (apply to every call):
+ *  - Ownership: the caller owns every array passed in or out.  Inputs are
+ *    copied during the call; no caller pointer is retained.  The context owns
+ *    its device buffers.
+ *  - Pointers marked "host or device" are classified with
+ *    cudaPointerGetAttributes; device pointers must live on the context's
+ *    device.  All other pointers are host pointers.
+ *  - Stream order: all device work is enqueued on the context stream (the one
+ *    passed to twg_create, e.g. torch.cuda.current_stream().cuda_stream).
+ *    A call that returns host data synchronises that stream before returning.
+ *  - Errors: a negative status means the call wrote no outputs (except where
+ *    stated); the message is available from twg_last_error.  Positive status
+ *    values are warnings; outputs are valid.  Nothing throws across the ABI.
+ *  - A context is single-owner; distinct contexts may be used
+ *    concurrently from different threads.
+ *  - Grid coordinates: cell (x, y), x = column in [0, width), y = row in
+ *    [0, height), row-major; world point p belongs to cell
+ *    floor((p - origin) / cell_size).
+ *  - Field encoding on the device ("raw u", used by twg_get_field(raw) and
+ *    twg_set_field): u = 1 - phi stored as fp32 (C3) with the sign bit as the
+ *    free/fixed flag: a free cell holding u >= 0 is stored as -u (sign bit
+ *    set); a fixed cell is stored non-negative: obstacle +0.0 (phi = 1),
+ *    goal +1.0 (phi = 0).  Any other non-negative value is a fixed Dirichlet
+ *    cell with that u (test data, pin P8).  Outside the grid u = +0.0
+ *    (obstacle, C4).
+ */
+#ifndef TWG_H
+#define TWG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+#define TWG_API extern "C" __attribute__((visibility("default")))
+#else
+#define TWG_API __attribute__((visibility("default")))
+#endif
+
+typedef struct twg_ctx twg_ctx; /* opaque; owns the device state of `batch` scenarios */
+typedef int32_t twg_status;
+
+enum {
+    TWG_OK = 0,
+    TWG_W_GOAL_SWALLOWED = 1,      /* a footprint covered the goal cell; the goal was kept */
+    TWG_W_TRUNCATED = 2,           /* smoothed path longer than max_smooth; output truncated */
+    TWG_E_INVALID_ARG = -1,
+    TWG_E_OUT_OF_BOUNDS = -2,      /* goal or robot cell outside the grid */
+    TWG_E_OVERLAPPING_CLASSES = -3,/* goal on a static wall */
+    TWG_E_INVALID_START = -4,      /* robot cell on a static wall */
+    TWG_E_NO_PATH = -5,            /* walk entered an obstacle or exceeded max_len (C9) */
+    TWG_E_CUDA = -6,
+    TWG_E_NCCL = -7,
+    TWG_E_NO_MEMORY = -8
+};
+
+/* Grid of `batch` independent scenarios of width x height cells of
+ * cell_size metres (0.1 m), cell (0,0)'s corner at (origin_x,
+ * origin_y).  row_offset: global index of local row 0 (row-slab sharding,
+ * DESIGN.md "Multi-GPU"); red/black colour = parity of (x + row_offset + y)
+ * (C1).  Single-GPU contexts pass 0. */
+typedef struct {
+    int32_t width, height, batch, row_offset;
+    double cell_size, origin_x, origin_y;
+} twg_grid_desc;
+
+/* Robot pose and speed: metres, metres, radians (heading theta of Eq. 14,
+ * P:462), m/s ("velocity of the robot"). */
+typedef struct {
+    double x, y, theta, speed;
+} twg_robot;
+
+/* Kalman track of one moving obstacle: state (x, y, vx, vy) in
+ * m and m/s and its 4x4 covariance P, row-major (Eq. 10). */
+typedef struct {
+    double x[4];
+    double P[16];
+} twg_track;
+
+/* Time-warp / predict configuration (defaults in brackets):
+ *   dt [0.1 s] Kalman step; Q [1e-3 diag(dt^4/4, dt^4/4, dt^2, dt^2), S:307]
+ *   process noise, row-major; warp_spacing [1.0 m] width of one warp ring
+ *   (C17); eps_v [0.05 m/s] obstacle-speed floor of Eq. 16 (C18);
+ *   safety_radius [0.5 m] (C20); horizon_max [20] clamp of j (C18). */
+typedef struct {
+    double dt;
+    double Q[16];
+    double warp_spacing;
+    double eps_v;
+    double safety_radius;
+    int32_t horizon_max;
+    int32_t reserved;
+} twg_warp_cfg;
+
+/* Relaxation control (rows a4-a6):
+ *   max_sweeps [100, Alg. 1 P:694]; check_every [max_sweeps]: the residual
+ *   max|du| of sweep s is evaluated when s % check_every == 0 or s ==
+ *   max_sweeps (C5); stop early when it is < tol (tol <= 0: fixed budget,
+ *   C6); warm_start [1]: used by twg_plan_step's encode (C7);
+ *   temporal_depth [0 = auto]: sweeps fused per tile load (T);
+ *   rows_per_warp [0 = auto]: rows of the strip one warp owns;
+ *   sync_every [64]: convergence flags are read back every sync_every
+ *   checks when tol > 0. */
+typedef struct {
+    int32_t max_sweeps, check_every, warm_start, temporal_depth;
+    float tol;
+    int32_t rows_per_warp, sync_every, reserved;
+} twg_relax_cfg;
+
+/* Path output control (rows a7-a9):
+ *   iterations [50] rubber-band iterations (C10); max_len: walk cells
+ *   capacity (NoPath beyond); max_smooth: smoothed points capacity;
+ *   step [0.25 cell] candidate offset (C12); k_t [1.0] tension constant (C11). */
+typedef struct {
+    int32_t iterations, max_len, max_smooth, reserved;
+    float step, k_t;
+} twg_band_cfg;
+
+/* Result of one planning tick.  next_x/next_y: next waypoint in cell units
+ * (cell (i, k) has centre (i + 0.5, k + 0.5)) (Alg. 1). */
+typedef struct {
+    twg_status status;      /* worst status of the tick (errors < 0 < warnings) */
+    int32_t sweeps;         /* sweeps performed */
+    int32_t n_cells;        /* descent-walk cells (0 on NoPath) */
+    int32_t n_smooth;       /* smoothed + resampled points (may exceed max_smooth: truncated) */
+    float residual;         /* max |du| of the last sweep (C5) */
+    float next_x, next_y;   /* next waypoint (cell units) */
+    int32_t walk_status;    /* TWG_OK or TWG_E_NO_PATH */
+} twg_plan_result;
+
+/* Create a context for `desc->batch` scenarios on CUDA device `device`,
+ * enqueuing on `cuda_stream` (a cudaStream_t; NULL = the legacy default
+ * stream).  Allocates 2 ping-pong fields of height x pitch fp32 per scenario
+ * (pitch = width rounded up to 32) plus a uint8 static mask.  Every field
+ * starts as all-free cold (u = 0.5) with no goal.
+ * Errors: INVALID_ARG (sizes <= 0, cell_size <= 0), CUDA, NO_MEMORY. */
+TWG_API twg_status twg_create(const twg_grid_desc* desc, int32_t device, void* cuda_stream, twg_ctx** out);
+
+/* Release all device memory of the context.  NULL is a no-op. */
+TWG_API twg_status twg_destroy(twg_ctx* ctx);
+
+/* Static wall mask of scenario b (b = -1: every scenario), height x width
+ * uint8 row-major, non-zero = wall ("phi(x,y) = 1"; P:586 red lines).
+ * Host or device pointer.  The next twg_set_obstacles re-encodes cold. */
+TWG_API twg_status twg_set_static(twg_ctx* ctx, int32_t b, const uint8_t* occ);
+
+/* Rows a1-a3 for scenario b (Alg. 1 Map Update):
+ *   a1 warp radius of each track from its current estimate (Eq. 15 closed
+ *      form, C16; warp number t, C17);
+ *   a2 horizon j = clamp(round(v t)) (Eq. 16, C18) and j Kalman predicts
+ *      (Eqs. 9-10) giving the footprint R^2 (C19, C20);
+ *   a3 field encode: cells whose centre lies within R of a predicted
+ *      position become obstacles, static walls stay obstacles, the goal cell
+ *      is the goal, the robot's cell stays free (C22).
+ * warm = 0: every free cell restarts at 0.5 ("cleared");
+ * warm = 1: free cells keep their value, cells fixed in the previous call
+ * and free now restart at 0.5 (C7).
+ * tracks: n entries, host or device pointer (n may be 0).
+ * Returns OK, W_GOAL_SWALLOWED, or OUT_OF_BOUNDS / OVERLAPPING_CLASSES /
+ * INVALID_START / INVALID_ARG (validated before any device work). */
+TWG_API twg_status twg_set_obstacles(twg_ctx* ctx, int32_t b, const twg_robot* robot,
+                                     int32_t goal_x, int32_t goal_y,
+                                     const twg_track* tracks, int32_t n,
+                                     const twg_warp_cfg* cfg, int32_t warm);
+
+/* Rows a4-a6 for every scenario: red-black Gauss-Seidel relaxation of
+ * Eq. 2 realised as red pass then black pass per sweep (C1),
+ * each free cell u <- 0.25 ((E + W) + (N + S)) (C2), with the residual
+ * and stop rule of cfg.  sweeps_done[batch] and residual[batch] are host
+ * arrays; if both are NULL and cfg->tol <= 0 the call does not synchronise.
+ * Errors: INVALID_ARG (max_sweeps < 0, check_every < 0), CUDA. */
+TWG_API twg_status twg_relax(twg_ctx* ctx, const twg_relax_cfg* cfg, int32_t* sweeps_done, float* residual);
+
+/* Rows a7-a9 for scenario b on the current field:
+ *   a7 descent walk from the robot cell of the last twg_set_obstacles along
+ *      the implicit index matrix of Eq. 3 (argmax u, order +x, -x, +y, -y,
+ *      first maximum wins, C8), into cells_xy (max_len (x, y) int32 pairs);
+ *   a8 rubber band (Eqs. 4-6, C10-C14) of the cell-centre waypoints, then
+ *      resampling (C15) into smooth_xy (max_smooth (x, y) float pairs);
+ *   a9 next waypoint into next_xy[2] (cell units).
+ * Host arrays; any output pointer may be NULL.  Returns OK, W_TRUNCATED or
+ * NO_PATH (then *n_cells = *n_smooth = 0 and next_xy = robot cell centre). */
+TWG_API twg_status twg_extract_path(twg_ctx* ctx, int32_t b, const twg_band_cfg* cfg,
+                                    int32_t* cells_xy, int32_t* n_cells,
+                                    float* smooth_xy, int32_t* n_smooth, float* next_xy);
+
+/* One planning tick (Algorithm 1) = twg_set_obstacles (warm =
+ * relax->warm_start) + twg_relax + twg_extract_path.
+ * b >= 0: scenario b; robot, goal_xy[2], tracks[n_tracks[0]], out[1],
+ *   cells_xy[2 max_len], smooth_xy[2 max_smooth].
+ * b = -1: every scenario; robot[batch], goal_xy[2 batch], tracks = the
+ *   concatenation of n_tracks[0..batch) tracks, out[batch],
+ *   cells_xy[batch][2 max_len], smooth_xy[batch][2 max_smooth].
+ * tracks may be host or device; every other pointer is host (cells_xy,
+ * smooth_xy may be NULL).  Returns the worst per-scenario status. */
+TWG_API twg_status twg_plan_step(twg_ctx* ctx, int32_t b, const twg_robot* robot, const int32_t* goal_xy,
+                                 const twg_track* tracks, const int32_t* n_tracks,
+                                 const twg_warp_cfg* warp, const twg_relax_cfg* relax,
+                                 const twg_band_cfg* band, twg_plan_result* out,
+                                 int32_t* cells_xy, float* smooth_xy);
+
+/* Copy scenario b's current field (height x width fp32, row-major, no
+ * pitch) to `out` (host or device).  mode 0: raw u (header encoding);
+ * 1: |u| (u-space magnitudes); 2: phi = 1 - |u|. */
+TWG_API twg_status twg_get_field(twg_ctx* ctx, int32_t b, float* out, int32_t mode);
+
+/* Replace scenario b's current field by `raw` (height x width, raw u
+ * encoding, host or device) -- warm start / checkpoint restore / test data. */
+TWG_API twg_status twg_set_field(twg_ctx* ctx, int32_t b, const float* raw);
+
+/* Per-track results of the last twg_set_obstacles on scenario b (rows a1-a2,
+ * for parity tests): t[n] warp numbers, j[n] horizons, pred[3 n] =
+ * (x_pred, y_pred, R^2).  n must equal the track count of that call. */
+TWG_API twg_status twg_get_warp(twg_ctx* ctx, int32_t b, int32_t n, int32_t* t, int32_t* j, double* pred);
+
+/* Device pointer and pitch (floats) of scenario b's current field buffer
+ * (valid until the next call on ctx). */
+TWG_API twg_status twg_field_ptr(twg_ctx* ctx, int32_t b, void** dev_ptr, int64_t* pitch);
+
+/* Kernel-level accounting for bench.py: total kernel launches enqueued by
+ * this context since creation, and, while profiling is enabled, CUDA-event
+ * time and launch count of the relaxation tile kernel (the dominant kernel),
+ * plus the lattice updates those launches performed. */
+TWG_API int64_t twg_kernel_launches(const twg_ctx* ctx);
+TWG_API twg_status twg_profile(twg_ctx* ctx, int32_t enable);
+TWG_API twg_status twg_profile_read(twg_ctx* ctx, double* relax_ms, int64_t* relax_launches, int64_t* cell_sweeps);
+
+/* Message of the last error on ctx ("" if none); ctx NULL: last twg_create error. */
+TWG_API const char* twg_last_error(const twg_ctx* ctx);
+
+#endif /* TWG_H */

@@ -1,0 +1,839 @@
+// api.cu -- the C ABI of include/twg.h: validation, host-side trig, H2D/D2H, buffer
+// management and kernel orchestration.  Every step of the hot path runs in the
+// kernels of k_stamp.cu (a1-a3), k_relax.cu (a4-a6) and k_path.cu (a7-a9).
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "twg_kernels.cuh"
+
+using namespace twg;
+
+namespace {
+
+std::string g_create_err;
+
+twg_status fail(twg_ctx* c, twg_status st, const std::string& msg) {
+    if (c) c->err = msg;
+    else g_create_err = msg;
+    return st;
+}
+
+#define TWG_CUDA(ctx, expr)                                                                                 \
+    do {                                                                                                    \
+        cudaError_t e_ = (expr);                                                                            \
+        if (e_ != cudaSuccess)                                                                              \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? TWG_E_NO_MEMORY : TWG_E_CUDA,                \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                                \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    if (p == nullptr) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3D map {W, H, B} over one ping-pong buffer; box {128, kRingRows, 1}; OOB -> zero fill.
+bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+    cuuint64_t strides[2] = {(cuuint64_t)(P * 4), (cuuint64_t)(P * 4 * (int64_t)H)};
+    cuuint32_t box[3] = {(cuuint32_t)kStripW, (cuuint32_t)kRingRows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <class T>
+cudaError_t dev_alloc(T** p, size_t n) {
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T));
+}
+
+// Pinned host staging ring.  Regions are handed out in order; when the ring wraps
+// (or must grow) the stream is synchronised first, so a region is never rewritten
+// while an earlier asynchronous copy may still read it.
+cudaError_t stage_alloc(twg_ctx* c, size_t bytes, void** out) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes > c->h_stage_bytes) {
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) return e;
+        if (c->h_stage) cudaFreeHost(c->h_stage);
+        c->h_stage = nullptr;
+        c->h_stage_bytes = 0;
+        const size_t nb = std::max<size_t>(bytes, size_t(8) << 20);
+        e = cudaMallocHost(&c->h_stage, nb);
+        if (e != cudaSuccess) return e;
+        c->h_stage_bytes = nb;
+        c->stage_off = 0;
+    } else if (c->stage_off + bytes > c->h_stage_bytes) {
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) return e;
+        c->stage_off = 0;
+    }
+    *out = static_cast<char*>(c->h_stage) + c->stage_off;
+    c->stage_off += bytes;
+    return cudaSuccess;
+}
+
+// Grow the per-scenario track arrays to `cap` entries, keeping their contents.
+twg_status ensure_track_cap(twg_ctx* c, int cap) {
+    if (cap <= c->track_cap) return TWG_OK;
+    int nc = std::max(cap, std::max(2 * c->track_cap, 64));
+    const size_t B = c->B;
+    twg_track* t0;
+    int *t1, *t2;
+    double* t3;
+    int4* t4;
+    TWG_CUDA(c, dev_alloc(&t0, B * nc));
+    TWG_CUDA(c, dev_alloc(&t1, B * nc));
+    TWG_CUDA(c, dev_alloc(&t2, B * nc));
+    TWG_CUDA(c, dev_alloc(&t3, B * nc * 3));
+    TWG_CUDA(c, dev_alloc(&t4, B * nc));
+    if (c->track_cap > 0) {
+        const int oc = c->track_cap;
+        TWG_CUDA(c, cudaMemcpy2DAsync(t0, nc * sizeof(twg_track), c->d_tracks, oc * sizeof(twg_track),
+                                      oc * sizeof(twg_track), B, cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaMemcpy2DAsync(t1, nc * sizeof(int), c->d_t, oc * sizeof(int), oc * sizeof(int), B,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaMemcpy2DAsync(t2, nc * sizeof(int), c->d_j, oc * sizeof(int), oc * sizeof(int), B,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaMemcpy2DAsync(t3, nc * 3 * sizeof(double), c->d_pred, oc * 3 * sizeof(double),
+                                      oc * 3 * sizeof(double), B, cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaMemcpy2DAsync(t4, nc * sizeof(int4), c->d_boxes, oc * sizeof(int4), oc * sizeof(int4), B,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+        cudaFree(c->d_tracks);
+        cudaFree(c->d_t);
+        cudaFree(c->d_j);
+        cudaFree(c->d_pred);
+        cudaFree(c->d_boxes);
+    }
+    c->d_tracks = t0;
+    c->d_t = t1;
+    c->d_j = t2;
+    c->d_pred = t3;
+    c->d_boxes = t4;
+    c->track_cap = nc;
+    return TWG_OK;
+}
+
+twg_status ensure_params(twg_ctx* c, int n) {
+    if (n <= c->params_cap) return TWG_OK;
+    if (c->d_params) cudaFree(c->d_params);
+    c->d_params = nullptr;
+    TWG_CUDA(c, dev_alloc(&c->d_params, n));
+    c->params_cap = n;
+    return TWG_OK;
+}
+
+twg_status ensure_path_cap(twg_ctx* c, int max_len, int max_smooth) {
+    const size_t B = c->B;
+    if (max_len > c->path_len_cap) {
+        int nc = std::max(max_len, 256);
+        if (c->d_cells) cudaFree(c->d_cells);
+        if (c->d_wp) cudaFree(c->d_wp);
+        c->d_cells = nullptr;
+        c->d_wp = nullptr;
+        TWG_CUDA(c, dev_alloc(&c->d_cells, B * nc));
+        TWG_CUDA(c, dev_alloc(&c->d_wp, B * nc));
+        c->path_len_cap = nc;
+    }
+    if (max_smooth > c->smooth_cap) {
+        int nc = std::max(max_smooth, 256);
+        if (c->d_smooth) cudaFree(c->d_smooth);
+        c->d_smooth = nullptr;
+        TWG_CUDA(c, dev_alloc(&c->d_smooth, B * nc));
+        c->smooth_cap = nc;
+    }
+    return TWG_OK;
+}
+
+twg_status check_ctx(twg_ctx* c) {
+    if (!c) return TWG_E_INVALID_ARG;
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(c, TWG_E_CUDA, cudaGetErrorString(e));
+    return TWG_OK;
+}
+
+// One scenario's encode request.
+struct EncodeReq {
+    int b;
+    twg_robot robot;
+    int gx, gy;
+    int n;
+    int64_t track_off;  // offset into the caller's track array
+};
+
+// Host validation -> robot cell.
+twg_status validate(twg_ctx* c, const EncodeReq& r, int* rcx, int* rcy) {
+    if (r.gx < 0 || r.gy < 0 || r.gx >= c->W || r.gy >= c->H)
+        return fail(c, TWG_E_OUT_OF_BOUNDS, "goal cell outside the grid");
+    const uint8_t* m = c->hmask.data() + (size_t)r.b * c->H * c->W;
+    if (m[(size_t)r.gy * c->W + r.gx]) return fail(c, TWG_E_OVERLAPPING_CLASSES, "goal cell on a static wall");
+    const double fx = std::floor((r.robot.x - c->ox) / c->cs), fy = std::floor((r.robot.y - c->oy) / c->cs);
+    if (!(fx >= 0.0 && fy >= 0.0 && fx < (double)c->W && fy < (double)c->H))
+        return fail(c, TWG_E_OUT_OF_BOUNDS, "robot cell outside the grid");
+    *rcx = (int)fx;
+    *rcy = (int)fy;
+    if (m[(size_t)*rcy * c->W + *rcx]) return fail(c, TWG_E_INVALID_START, "robot cell on a static wall");
+    if (r.n < 0) return fail(c, TWG_E_INVALID_ARG, "negative track count");
+    return TWG_OK;
+}
+
+// Rows a1-a3 for a list of scenarios.  tracks: concatenated per request (host or device).
+twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_track* tracks, const twg_warp_cfg* wc,
+                  int warm_req) {
+    if (!wc) return fail(c, TWG_E_INVALID_ARG, "null warp cfg");
+    const int ns = (int)reqs.size();
+    std::vector<ScenParams> ps(ns);
+    int max_n = 0, max_prev = 0, any_cold = 0;
+    int64_t total = 0;
+    for (int k = 0; k < ns; ++k) {
+        const EncodeReq& r = reqs[k];
+        int rcx, rcy;
+        twg_status st = validate(c, r, &rcx, &rcy);
+        if (st != TWG_OK) return st;
+        twg_ctx::Scen& sc = c->scen[r.b];
+        ScenParams& p = ps[k];
+        p.xr = r.robot.x;
+        p.yr = r.robot.y;
+        p.c = std::cos(r.robot.theta);  // host libm (C25)
+        p.s = std::sin(r.robot.theta);
+        p.speed = r.robot.speed;
+        p.b = r.b;
+        p.gx = r.gx;
+        p.gy = r.gy;
+        p.rcx = rcx;
+        p.rcy = rcy;
+        const bool warm = warm_req && sc.encoded && !sc.static_dirty;
+        p.warm = warm ? 1 : 0;
+        p.old_gx = warm ? sc.gx : -1;
+        p.old_gy = warm ? sc.gy : -1;
+        p.cur = c->cur[r.b];
+        p.n_tracks = r.n;
+        p.n_prev_boxes = warm ? sc.n_boxes : 0;
+        max_n = std::max(max_n, r.n);
+        max_prev = std::max(max_prev, p.n_prev_boxes);
+        any_cold |= !warm;
+        total += r.n;
+    }
+    twg_status st = ensure_track_cap(c, std::max(max_n, 1));
+    if (st != TWG_OK) return st;
+    st = ensure_params(c, ns);
+    if (st != TWG_OK) return st;
+    // tracks -> [B][cap]
+    if (total > 0) {
+        if (is_device_ptr(tracks)) {
+            std::vector<int> off(ns + 1), sb(ns);
+            for (int k = 0; k < ns; ++k) {
+                off[k] = (int)reqs[k].track_off;
+                sb[k] = reqs[k].b;
+            }
+            off[ns] = (int)(reqs[ns - 1].track_off + reqs[ns - 1].n);
+            if (c->track_off_cap < 2 * ns + 1) {
+                if (c->d_track_off) cudaFree(c->d_track_off);
+                c->d_track_off = nullptr;
+                TWG_CUDA(c, dev_alloc(&c->d_track_off, 2 * ns + 1));
+                c->track_off_cap = 2 * ns + 1;
+            }
+            int* hs = nullptr;
+            TWG_CUDA(c, stage_alloc(c, (2 * ns + 1) * sizeof(int), reinterpret_cast<void**>(&hs)));
+            std::memcpy(hs, off.data(), (ns + 1) * sizeof(int));
+            std::memcpy(hs + ns + 1, sb.data(), ns * sizeof(int));
+            TWG_CUDA(c, cudaMemcpyAsync(c->d_track_off, hs, (2 * ns + 1) * sizeof(int), cudaMemcpyHostToDevice,
+                                        c->stream));
+            TWG_CUDA(c, launch_scatter_tracks(tracks, c->d_track_off, ns, c->d_track_off + ns + 1, c->d_tracks,
+                                              c->track_cap, c->stream));
+            c->launches += 1;
+        } else {
+            for (int k = 0; k < ns; ++k)
+                if (reqs[k].n > 0)
+                    TWG_CUDA(c, cudaMemcpyAsync(c->d_tracks + (int64_t)reqs[k].b * c->track_cap,
+                                                tracks + reqs[k].track_off, reqs[k].n * sizeof(twg_track),
+                                                cudaMemcpyHostToDevice, c->stream));
+        }
+    }
+    // per-scenario params + cfg (pinned staging, one copy each)
+    WarpCfgDev w;
+    w.dt = wc->dt;
+    std::memcpy(w.Q, wc->Q, sizeof(w.Q));
+    w.w = wc->warp_spacing;
+    w.eps_v = wc->eps_v;
+    w.rs = wc->safety_radius;
+    w.hmax = wc->horizon_max;
+    const size_t pbytes = ns * sizeof(ScenParams);
+    char* hs = nullptr;
+    TWG_CUDA(c, stage_alloc(c, pbytes + sizeof(WarpCfgDev) + 64, reinterpret_cast<void**>(&hs)));
+    std::memcpy(hs, ps.data(), pbytes);
+    std::memcpy(hs + pbytes, &w, sizeof(w));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_params, hs, pbytes, cudaMemcpyHostToDevice, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_wcfg, hs + pbytes, sizeof(w), cudaMemcpyHostToDevice, c->stream));
+    // clear warning flags of these scenarios
+    for (int k = 0; k < ns; ++k) TWG_CUDA(c, cudaMemsetAsync(c->d_flags + reqs[k].b, 0, sizeof(int), c->stream));
+    EncodeArgs e;
+    e.u0 = c->u[0];
+    e.u1 = c->u[1];
+    e.P = c->P;
+    e.sstride = c->sstride;
+    e.W = c->W;
+    e.H = c->H;
+    e.mask = c->mask;
+    e.params = c->d_params;
+    e.nscen = ns;
+    e.wcfg = c->d_wcfg;
+    e.tracks = c->d_tracks;
+    e.cap = c->track_cap;
+    e.t_out = c->d_t;
+    e.j_out = c->d_j;
+    e.pred = c->d_pred;
+    e.boxes = c->d_boxes;
+    e.flags = c->d_flags;
+    e.cs = c->cs;
+    e.ox = c->ox;
+    e.oy = c->oy;
+    int nl = 0;
+    TWG_CUDA(c, launch_encode(e, max_prev, max_n, any_cold, &nl, c->stream));
+    c->launches += nl;
+    // host-side bookkeeping for the next warm encode
+    for (int k = 0; k < ns; ++k) {
+        twg_ctx::Scen& sc = c->scen[reqs[k].b];
+        sc.gx = ps[k].gx;
+        sc.gy = ps[k].gy;
+        sc.rcx = ps[k].rcx;
+        sc.rcy = ps[k].rcy;
+        sc.n_tracks = reqs[k].n;
+        sc.n_boxes = reqs[k].n;
+        sc.encoded = true;
+        sc.static_dirty = false;
+    }
+    return TWG_OK;
+}
+
+int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows) {
+    int h;
+    if (cfg_rows > 0) {
+        h = cfg_rows;
+    } else {
+        const int target = 148 * 16;  // warps in flight per launch (4 CTAs x 4 warps per SM)
+        int segs = (target + n_strips * nscen - 1) / (n_strips * nscen);
+        segs = std::max(segs, 1);
+        h = (H + segs - 1) / segs;
+        h = std::max(h, 8 * T);
+    }
+    h = std::min(h, H);
+    h = (h + 1) & ~1;  // even (red/black parity of the first row)
+    return std::max(h, 2);
+}
+
+// Rows a4-a6 for the scenarios whose participation flag is set.
+twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& part, int* sweeps_done,
+                 float* residual) {
+    if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null relax cfg");
+    const int maxs = cfg->max_sweeps;
+    if (maxs < 0 || cfg->check_every < 0) return fail(c, TWG_E_INVALID_ARG, "negative sweep counts");
+    const int B = c->B;
+    int T = cfg->temporal_depth > 0 ? std::min(cfg->temporal_depth, kMaxT) : 4;
+    const float tol = cfg->tol;
+    int check = (tol > 0.0f && cfg->check_every > 0) ? cfg->check_every : std::max(maxs, 1);
+    const int sync_every = cfg->sync_every > 0 ? cfg->sync_every : 64;
+    // control arrays: done = !participating; sweeps = 0; residual bits = 0; cur uploaded
+    int* hs = nullptr;
+    TWG_CUDA(c, stage_alloc(c, 2 * B * sizeof(int), reinterpret_cast<void**>(&hs)));
+    for (int b = 0; b < B; ++b) {
+        hs[b] = part[b] ? 0 : 1;
+        hs[B + b] = c->cur[b];
+    }
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_done, hs, B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_cur, hs + B, B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    TWG_CUDA(c, cudaMemsetAsync(c->d_sweeps, 0, B * sizeof(int), c->stream));
+    TWG_CUDA(c, cudaMemsetAsync(c->d_res_bits, 0, B * sizeof(unsigned), c->stream));
+    TWG_CUDA(c, cudaMemsetAsync(c->d_res, 0, B * sizeof(float), c->stream));
+    int nscen = 0;
+    for (int b = 0; b < B; ++b) nscen += part[b] ? 1 : 0;
+
+    int lp = 0;  // launches so far (parity)
+    if (maxs > 0) {
+        RelaxArgs a;
+        a.u0 = c->u[0];
+        a.u1 = c->u[1];
+        a.cur = c->d_cur;
+        a.P = c->P;
+        a.sstride = c->sstride;
+        a.W = c->W;
+        a.H = c->H;
+        a.done = c->d_done;
+        a.res = c->d_res_bits;
+        const int qoff = c->row_off & 1;
+        int done_sw = 0, nchunk = 0;
+        while (done_sw < maxs) {
+            const int chunk = std::min(check, maxs - done_sw);
+            // launches of T sweeps; the remainder first; the last launch accumulates the residual
+            std::vector<int> plan;
+            if (chunk % T) plan.push_back(chunk % T);
+            for (int q = 0; q < chunk / T; ++q) plan.push_back(T);
+            for (size_t q = 0; q < plan.size(); ++q) {
+                const int t = plan[q];
+                a.n_strips = (c->W + out_cols(t) - 1) / out_cols(t);
+                a.hseg = auto_hseg(t, c->H, a.n_strips, std::max(nscen, 1), cfg->rows_per_warp);
+                a.seg_begin = 0;
+                a.seg_end = (c->H + a.hseg - 1) / a.hseg;
+                a.lp = lp & 1;
+                cudaEvent_t e0 = nullptr, e1 = nullptr;
+                if (c->prof) {
+                    while ((int)c->ev_pool.size() < c->ev_used + 2) {
+                        cudaEvent_t ev;
+                        TWG_CUDA(c, cudaEventCreate(&ev));
+                        c->ev_pool.push_back(ev);
+                    }
+                    e0 = c->ev_pool[c->ev_used++];
+                    e1 = c->ev_pool[c->ev_used++];
+                    TWG_CUDA(c, cudaEventRecord(e0, c->stream));
+                }
+                TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0], c->tmap[1], a, B, qoff, q + 1 == plan.size(), c->stream));
+                if (c->prof) {
+                    TWG_CUDA(c, cudaEventRecord(e1, c->stream));
+                    c->prof_launches += 1;
+                    c->prof_cells += (int64_t)nscen * c->W * c->H * t;
+                }
+                c->launches += 1;
+                ++lp;
+            }
+            TWG_CUDA(c, launch_check(B, c->d_done, c->d_sweeps, c->d_res_bits, c->d_res, c->d_where, chunk, check, maxs,
+                                     tol, c->d_cur, lp & 1, c->stream));
+            c->launches += 1;
+            done_sw += chunk;
+            ++nchunk;
+            if (tol > 0.0f && done_sw < maxs && nchunk % sync_every == 0) {
+                int* hd = nullptr;
+                TWG_CUDA(c, stage_alloc(c, B * sizeof(int), reinterpret_cast<void**>(&hd)));
+                TWG_CUDA(c, cudaMemcpyAsync(hd, c->d_done, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+                TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+                bool all = true;
+                for (int b = 0; b < B; ++b) all = all && hd[b];
+                if (all) break;
+            }
+        }
+        TWG_CUDA(c, launch_fixup(c->u[0], c->u[1], c->sstride, B, c->d_where, c->d_cur, lp & 1, c->stream));
+        c->launches += 1;
+        for (int b = 0; b < B; ++b)
+            if (part[b]) c->cur[b] ^= (lp & 1);
+    }
+    if (sweeps_done || residual) {
+        int* hsw = nullptr;
+        TWG_CUDA(c, stage_alloc(c, 2 * B * sizeof(int), reinterpret_cast<void**>(&hsw)));
+        float* hr = reinterpret_cast<float*>(hsw + B);
+        TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        TWG_CUDA(c, cudaMemcpyAsync(hr, c->d_res, B * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+        for (int b = 0; b < B; ++b) {
+            if (sweeps_done) sweeps_done[b] = hsw[b];
+            if (residual) residual[b] = hr[b];
+        }
+    }
+    return TWG_OK;
+}
+
+// Rows a7-a9 for a list of scenarios (path kernels only; results stay on device).
+twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg) {
+    if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null band cfg");
+    if (cfg->max_len < 1 || cfg->max_smooth < 1 || cfg->iterations < 0)
+        return fail(c, TWG_E_INVALID_ARG, "band cfg: max_len, max_smooth >= 1, iterations >= 0");
+    twg_status st = ensure_path_cap(c, cfg->max_len, cfg->max_smooth);
+    if (st != TWG_OK) return st;
+    const int ns = (int)bs.size();
+    st = ensure_params(c, ns);
+    if (st != TWG_OK) return st;
+    std::vector<ScenParams> ps(ns);
+    for (int k = 0; k < ns; ++k) {
+        const twg_ctx::Scen& sc = c->scen[bs[k]];
+        if (!sc.encoded) return fail(c, TWG_E_INVALID_ARG, "extract_path before set_obstacles");
+        std::memset(&ps[k], 0, sizeof(ScenParams));
+        ps[k].b = bs[k];
+        ps[k].gx = sc.gx;
+        ps[k].gy = sc.gy;
+        ps[k].rcx = sc.rcx;
+        ps[k].rcy = sc.rcy;
+        ps[k].cur = c->cur[bs[k]];
+    }
+    void* hp = nullptr;
+    TWG_CUDA(c, stage_alloc(c, ns * sizeof(ScenParams), &hp));
+    std::memcpy(hp, ps.data(), ns * sizeof(ScenParams));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_params, hp, ns * sizeof(ScenParams), cudaMemcpyHostToDevice, c->stream));
+    PathArgs p;
+    p.u0 = c->u[0];
+    p.u1 = c->u[1];
+    p.P = c->P;
+    p.sstride = c->sstride;
+    p.W = c->W;
+    p.H = c->H;
+    p.params = c->d_params;
+    p.nscen = ns;
+    p.max_len = cfg->max_len;
+    p.max_smooth = cfg->max_smooth;
+    p.iters = cfg->iterations;
+    p.step = cfg->step;
+    p.kt = cfg->k_t;
+    p.cells = c->d_cells;
+    p.wp = c->d_wp;
+    p.smooth = c->d_smooth;
+    p.len_cap = c->path_len_cap;
+    p.smooth_cap = c->smooth_cap;
+    p.meta = c->d_meta;
+    int nl = 0;
+    TWG_CUDA(c, launch_path(p, &nl, c->stream));
+    c->launches += nl;
+    return TWG_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stream, twg_ctx** out) {
+    if (!d || !out) return fail(nullptr, TWG_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    if (d->width <= 0 || d->height <= 0 || d->batch <= 0 || !(d->cell_size > 0.0))
+        return fail(nullptr, TWG_E_INVALID_ARG, "width, height, batch > 0 and cell_size > 0 required");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(nullptr, TWG_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    twg_ctx* c = new twg_ctx();
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->W = d->width;
+    c->H = d->height;
+    c->B = d->batch;
+    c->row_off = d->row_offset;
+    c->cs = d->cell_size;
+    c->ox = d->origin_x;
+    c->oy = d->origin_y;
+    c->P = ((int64_t)c->W + 31) / 32 * 32;
+    c->sstride = c->P * c->H;
+    c->cur.assign(c->B, 0);
+    c->scen.assign(c->B, twg_ctx::Scen());
+    const size_t B = c->B, cells = (size_t)c->sstride * B;
+    auto bail = [&](twg_status st, const std::string& m) {
+        g_create_err = m;
+        twg_destroy(c);
+        return st;
+    };
+#define CK(expr)                                                                                      \
+    do {                                                                                              \
+        cudaError_t e_ = (expr);                                                                      \
+        if (e_ != cudaSuccess)                                                                        \
+            return bail(e_ == cudaErrorMemoryAllocation ? TWG_E_NO_MEMORY : TWG_E_CUDA,               \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                          \
+    } while (0)
+    CK(dev_alloc(&c->u[0], cells));
+    CK(dev_alloc(&c->u[1], cells));
+    CK(dev_alloc(&c->mask, B * c->H * c->W));
+    CK(dev_alloc(&c->d_done, B));
+    CK(dev_alloc(&c->d_sweeps, B));
+    CK(dev_alloc(&c->d_res_bits, B));
+    CK(dev_alloc(&c->d_res, B));
+    CK(dev_alloc(&c->d_where, B));
+    CK(dev_alloc(&c->d_cur, B));
+    CK(dev_alloc(&c->d_flags, B));
+    CK(dev_alloc(&c->d_meta, B));
+    CK(dev_alloc(&c->d_wcfg, 1));
+    CK(cudaMemsetAsync(c->mask, 0, B * c->H * c->W, c->stream));
+    CK(cudaMemsetAsync(c->d_meta, 0, B * sizeof(PathMeta), c->stream));
+    CK(launch_init_field(c->u[0], c->P, c->sstride, c->W, c->H, c->B, c->stream));
+    CK(launch_init_field(c->u[1], c->P, c->sstride, c->W, c->H, c->B, c->stream));
+    c->launches += 2;
+    c->hmask.assign(B * c->H * c->W, 0);
+    if (!make_tmap(&c->tmap[0], c->u[0], c->W, c->H, c->B, c->P) ||
+        !make_tmap(&c->tmap[1], c->u[1], c->W, c->H, c->B, c->P))
+        return bail(TWG_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point unavailable or bad layout)");
+    CK(cudaStreamSynchronize(c->stream));
+#undef CK
+    *out = c;
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_destroy(twg_ctx* c) {
+    if (!c) return TWG_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_done,  c->d_sweeps, c->d_res_bits, c->d_res,
+                    c->d_where,  c->d_cur,     c->d_flags, c->d_meta,  c->d_wcfg,   c->d_tracks,   c->d_t,
+                    c->d_j,      c->d_pred,    c->d_boxes, c->d_params, c->d_track_off, c->d_cells, c->d_wp,
+                    c->d_smooth};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    delete c;
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_set_static(twg_ctx* c, int32_t b, const uint8_t* occ) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!occ || b < -1 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad scenario index or null mask");
+    const size_t n = (size_t)c->H * c->W;
+    const bool dev = is_device_ptr(occ);
+    const int b0 = b < 0 ? 0 : b, b1 = b < 0 ? c->B : b + 1;
+    for (int q = b0; q < b1; ++q) {
+        if (dev) {
+            TWG_CUDA(c, cudaMemcpyAsync(c->mask + q * n, occ, n, cudaMemcpyDeviceToDevice, c->stream));
+            TWG_CUDA(c, cudaMemcpyAsync(c->hmask.data() + q * n, occ, n, cudaMemcpyDeviceToHost, c->stream));
+        } else {
+            std::memcpy(c->hmask.data() + q * n, occ, n);
+            TWG_CUDA(c, cudaMemcpyAsync(c->mask + q * n, c->hmask.data() + q * n, n, cudaMemcpyHostToDevice, c->stream));
+        }
+        c->scen[q].static_dirty = true;
+    }
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_set_obstacles(twg_ctx* c, int32_t b, const twg_robot* robot, int32_t goal_x, int32_t goal_y,
+                                     const twg_track* tracks, int32_t n, const twg_warp_cfg* cfg, int32_t warm) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!robot || b < 0 || b >= c->B || (n > 0 && !tracks)) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    EncodeReq r{b, *robot, goal_x, goal_y, n, 0};
+    st = encode(c, {r}, tracks, cfg, warm);
+    if (st != TWG_OK) return st;
+    int* hf = nullptr;
+    TWG_CUDA(c, stage_alloc(c, sizeof(int), reinterpret_cast<void**>(&hf)));
+    TWG_CUDA(c, cudaMemcpyAsync(hf, c->d_flags + b, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    const int flag = *hf;
+    return flag ? TWG_W_GOAL_SWALLOWED : TWG_OK;
+}
+
+TWG_API twg_status twg_relax(twg_ctx* c, const twg_relax_cfg* cfg, int32_t* sweeps_done, float* residual) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    std::vector<int> part(c->B, 1);
+    return relax(c, cfg, part, sweeps_done, residual);
+}
+
+TWG_API twg_status twg_extract_path(twg_ctx* c, int32_t b, const twg_band_cfg* cfg, int32_t* cells_xy,
+                                    int32_t* n_cells, float* smooth_xy, int32_t* n_smooth, float* next_xy) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad scenario index");
+    st = path(c, {b}, cfg);
+    if (st != TWG_OK) return st;
+    PathMeta* hm = nullptr;
+    TWG_CUDA(c, stage_alloc(c, sizeof(PathMeta), reinterpret_cast<void**>(&hm)));
+    TWG_CUDA(c, cudaMemcpyAsync(hm, c->d_meta + b, sizeof(PathMeta), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    const PathMeta m = *hm;
+    if (cells_xy && m.n_cells > 0)
+        TWG_CUDA(c, cudaMemcpyAsync(cells_xy, c->d_cells + (int64_t)b * c->path_len_cap, m.n_cells * sizeof(int2),
+                                    cudaMemcpyDeviceToHost, c->stream));
+    const int ns = std::min(m.n_smooth, cfg->max_smooth);
+    if (smooth_xy && ns > 0)
+        TWG_CUDA(c, cudaMemcpyAsync(smooth_xy, c->d_smooth + (int64_t)b * c->smooth_cap, ns * sizeof(float2),
+                                    cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (n_cells) *n_cells = m.n_cells;
+    if (n_smooth) *n_smooth = m.n_smooth;
+    if (next_xy) {
+        next_xy[0] = m.next_x;
+        next_xy[1] = m.next_y;
+    }
+    if (m.status != TWG_OK) return fail(c, TWG_E_NO_PATH, "no path: the walk entered an obstacle or exceeded max_len");
+    return m.n_smooth > cfg->max_smooth ? TWG_W_TRUNCATED : TWG_OK;
+}
+
+TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, const int32_t* goal_xy,
+                                 const twg_track* tracks, const int32_t* n_tracks, const twg_warp_cfg* warp,
+                                 const twg_relax_cfg* rcfg, const twg_band_cfg* bcfg, twg_plan_result* out,
+                                 int32_t* cells_xy, float* smooth_xy) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!robot || !goal_xy || !n_tracks || !rcfg || !bcfg || !out || b < -1 || b >= c->B)
+        return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    std::vector<EncodeReq> reqs;
+    std::vector<int> bs;
+    int64_t off = 0;
+    const int ns = b < 0 ? c->B : 1;
+    for (int k = 0; k < ns; ++k) {
+        EncodeReq r{b < 0 ? k : b, robot[k], goal_xy[2 * k], goal_xy[2 * k + 1], n_tracks[k], off};
+        off += n_tracks[k];
+        reqs.push_back(r);
+        bs.push_back(r.b);
+    }
+    if (off > 0 && !tracks) return fail(c, TWG_E_INVALID_ARG, "null tracks");
+    st = encode(c, reqs, tracks, warp, rcfg->warm_start);
+    if (st != TWG_OK) return st;
+    std::vector<int> part(c->B, 0);
+    for (int q : bs) part[q] = 1;
+    st = relax(c, rcfg, part, nullptr, nullptr);
+    if (st != TWG_OK) return st;
+    st = path(c, bs, bcfg);
+    if (st != TWG_OK) return st;
+    // D2H: per scenario meta, sweeps, residual, flags (pinned staging), then the paths
+    const int B = c->B;
+    const size_t mb = B * sizeof(PathMeta);
+    char* h = nullptr;
+    TWG_CUDA(c, stage_alloc(c, mb + 3 * B * sizeof(int), reinterpret_cast<void**>(&h)));
+    PathMeta* hm = reinterpret_cast<PathMeta*>(h);
+    int* hsw = reinterpret_cast<int*>(h + mb);
+    float* hr = reinterpret_cast<float*>(hsw + B);
+    int* hf = hsw + 2 * B;
+    TWG_CUDA(c, cudaMemcpyAsync(hm, c->d_meta, mb, cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(hr, c->d_res, B * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(hf, c->d_flags, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (cells_xy) {
+        if (b >= 0)
+            TWG_CUDA(c, cudaMemcpyAsync(cells_xy, c->d_cells + (int64_t)b * c->path_len_cap,
+                                        bcfg->max_len * sizeof(int2), cudaMemcpyDeviceToHost, c->stream));
+        else
+            TWG_CUDA(c, cudaMemcpy2DAsync(cells_xy, bcfg->max_len * sizeof(int2), c->d_cells,
+                                          c->path_len_cap * sizeof(int2), bcfg->max_len * sizeof(int2), B,
+                                          cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (smooth_xy) {
+        if (b >= 0)
+            TWG_CUDA(c, cudaMemcpyAsync(smooth_xy, c->d_smooth + (int64_t)b * c->smooth_cap,
+                                        bcfg->max_smooth * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
+        else
+            TWG_CUDA(c, cudaMemcpy2DAsync(smooth_xy, bcfg->max_smooth * sizeof(float2), c->d_smooth,
+                                          c->smooth_cap * sizeof(float2), bcfg->max_smooth * sizeof(float2), B,
+                                          cudaMemcpyDeviceToHost, c->stream));
+    }
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    twg_status worst = TWG_OK;
+    for (int k = 0; k < ns; ++k) {
+        const int q = bs[k];
+        twg_plan_result& r = out[k];
+        r.sweeps = hsw[q];
+        r.residual = hr[q];
+        r.n_cells = hm[q].n_cells;
+        r.n_smooth = hm[q].status == TWG_OK ? hm[q].n_smooth : 0;
+        r.next_x = hm[q].next_x;
+        r.next_y = hm[q].next_y;
+        r.walk_status = hm[q].status;
+        twg_status s = TWG_OK;
+        if (hm[q].status != TWG_OK) s = TWG_E_NO_PATH;
+        else if (hf[q]) s = TWG_W_GOAL_SWALLOWED;
+        else if (r.n_smooth > bcfg->max_smooth) s = TWG_W_TRUNCATED;
+        r.status = s;
+        if (s < 0 ? (worst >= 0 || s < worst) : (worst >= 0 && s > worst)) worst = s;
+    }
+    if (worst < 0) c->err = "at least one scenario has no path";
+    return worst;
+}
+
+TWG_API twg_status twg_get_field(twg_ctx* c, int32_t b, float* out, int32_t mode) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!out || b < 0 || b >= c->B || mode < 0 || mode > 2) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    const float* src = c->u[c->cur[b]] + (int64_t)b * c->sstride;
+    const size_t bytes = (size_t)c->W * c->H * sizeof(float);
+    if (is_device_ptr(out)) {
+        TWG_CUDA(c, launch_convert(src, c->P, c->W, c->H, out, mode, c->stream));
+        c->launches += 1;
+        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+        return TWG_OK;
+    }
+    float* tmp = nullptr;
+    TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&tmp), bytes, c->stream));
+    TWG_CUDA(c, launch_convert(src, c->P, c->W, c->H, tmp, mode, c->stream));
+    c->launches += 1;
+    TWG_CUDA(c, cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaFreeAsync(tmp, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_set_field(twg_ctx* c, int32_t b, const float* raw) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!raw || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    float* dst = c->u[c->cur[b]] + (int64_t)b * c->sstride;
+    const size_t bytes = (size_t)c->W * c->H * sizeof(float);
+    const float* src = raw;
+    float* tmp = nullptr;
+    if (!is_device_ptr(raw)) {
+        TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&tmp), bytes, c->stream));
+        TWG_CUDA(c, cudaMemcpyAsync(tmp, raw, bytes, cudaMemcpyHostToDevice, c->stream));
+        src = tmp;
+    }
+    TWG_CUDA(c, launch_import(src, c->W, c->H, dst, c->P, c->stream));
+    c->launches += 1;
+    if (tmp) TWG_CUDA(c, cudaFreeAsync(tmp, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_get_warp(twg_ctx* c, int32_t b, int32_t n, int32_t* t, int32_t* j, double* pred) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (b < 0 || b >= c->B || n != c->scen[b].n_tracks) return fail(c, TWG_E_INVALID_ARG, "bad scenario or count");
+    if (n == 0) return TWG_OK;
+    const int64_t o = (int64_t)b * c->track_cap;
+    if (t) TWG_CUDA(c, cudaMemcpyAsync(t, c->d_t + o, n * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (j) TWG_CUDA(c, cudaMemcpyAsync(j, c->d_j + o, n * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (pred) TWG_CUDA(c, cudaMemcpyAsync(pred, c->d_pred + 3 * o, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_field_ptr(twg_ctx* c, int32_t b, void** dev_ptr, int64_t* pitch) {
+    if (!c || b < 0 || b >= c->B) return TWG_E_INVALID_ARG;
+    if (dev_ptr) *dev_ptr = c->u[c->cur[b]] + (int64_t)b * c->sstride;
+    if (pitch) *pitch = c->P;
+    return TWG_OK;
+}
+
+TWG_API int64_t twg_kernel_launches(const twg_ctx* c) { return c ? c->launches : 0; }
+
+TWG_API twg_status twg_profile(twg_ctx* c, int32_t enable) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->prof = enable != 0;
+    c->ev_used = 0;
+    c->prof_launches = 0;
+    c->prof_cells = 0;
+    c->prof_ms = 0.0;
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_profile_read(twg_ctx* c, double* relax_ms, int64_t* relax_launches, int64_t* cell_sweeps) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    double ms = 0.0;
+    for (int q = 0; q + 1 < c->ev_used; q += 2) {
+        float e = 0.f;
+        TWG_CUDA(c, cudaEventElapsedTime(&e, c->ev_pool[q], c->ev_pool[q + 1]));
+        ms += e;
+    }
+    if (relax_ms) *relax_ms = ms;
+    if (relax_launches) *relax_launches = c->prof_launches;
+    if (cell_sweeps) *cell_sweeps = c->prof_cells;
+    return TWG_OK;
+}
+
+TWG_API const char* twg_last_error(const twg_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }

@@ -1,0 +1,293 @@
+// k_relax.cu -- rows a4-a6: red-black Laplace relaxation (Eq. 2, realised as
+// red-black Gauss-Seidel, C1), the fused max|du| residual (C5) and device-side
+// convergence control (C6).
+//
+// k_rb_tblock<T>: temporally blocked tile kernel.  One warp owns a strip of 128
+// columns (4 cells per lane) x hseg output rows.  Input rows arrive through a
+// per-warp TMA ring (cp.async.bulk.tensor.3d + mbarrier, OOB zero fill = the
+// outside-obstacle boundary C4); the 2T half-sweeps of T sweeps run as a
+// register wavefront: when row y lands, half-sweep k (k = 1..2T) updates row
+// y - k, so every input cell is read from HBM once per launch and written once
+// (8 B per cell per launch), while T lattice updates are performed per cell.
+// Halo: 2T rows above/below and round_up(2T, 4) columns left/right are
+// recomputed redundantly (SURVEY 0 finding 6).
+//
+// Bit-exactness with the oracle (oracle/twg_oracle.c orc_relax_f32): each free
+// cell becomes 0.25f * ((|E| + |W|) + (|N| + |S|)) -- the same IEEE operation
+// sequence (C2; the library is compiled with -fmad=false, no fast-math, no
+// FTZ); colours are global (x + row_offset + y) parity; the residual is the
+// exact max of fabsf(new - old) over the free cells of the last sweep.
+#include "twg_kernels.cuh"
+
+namespace twg {
+
+// Update the cells of parity q (j = q, q + 2 of the lane's float4) of row `c`
+// from rows `up` (y - 1) and `dn` (y + 1).  Returns the largest |du| of the
+// updated free cells in *dmax when TRACK.
+template <int Q, bool TRACK>
+__device__ __forceinline__ void half_sweep(float4& c, const float4& up, const float4& dn, float& dmax) {
+    if (Q == 0) {
+        const float l = __shfl_up_sync(0xffffffffu, c.w, 1);  // cell x - 1 of j = 0 (lane - 1, j = 3)
+        const float n0 = 0.25f * ((fabsf(c.y) + fabsf(l)) + (fabsf(up.x) + fabsf(dn.x)));
+        const float n2 = 0.25f * ((fabsf(c.w) + fabsf(c.y)) + (fabsf(up.z) + fabsf(dn.z)));
+        const bool f0 = is_free(c.x), f2 = is_free(c.z);
+        if (TRACK) {
+            if (f0) dmax = fmaxf(dmax, fabsf(-n0 - c.x));
+            if (f2) dmax = fmaxf(dmax, fabsf(-n2 - c.z));
+        }
+        c.x = f0 ? -n0 : c.x;
+        c.z = f2 ? -n2 : c.z;
+    } else {
+        const float r = __shfl_down_sync(0xffffffffu, c.x, 1);  // cell x + 1 of j = 3 (lane + 1, j = 0)
+        const float n1 = 0.25f * ((fabsf(c.z) + fabsf(c.x)) + (fabsf(up.y) + fabsf(dn.y)));
+        const float n3 = 0.25f * ((fabsf(r) + fabsf(c.z)) + (fabsf(up.w) + fabsf(dn.w)));
+        const bool f1 = is_free(c.y), f3 = is_free(c.w);
+        if (TRACK) {
+            if (f1) dmax = fmaxf(dmax, fabsf(-n1 - c.y));
+            if (f3) dmax = fmaxf(dmax, fabsf(-n3 - c.w));
+        }
+        c.y = f1 ? -n1 : c.y;
+        c.w = f3 ? -n3 : c.w;
+    }
+}
+
+// One wavefront step: row i of the strip (global row y = ystart + i) has landed in
+// win[S]; run half-sweeps k = 1..2T on rows y - k; store row y - 2T.
+template <int T, int QOFF, bool RESID, int S>
+__device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, int hs, bool lane_out,
+                                          float* __restrict__ out_row0, int64_t P, float& dmax) {
+    constexpr int NW = 2 * T + 2;
+    // all half-sweeps of this step update cells of one parity: q = (y + row_offset + 1) & 1
+    constexpr int Qp = (S + 1 + QOFF) & 1;
+#pragma unroll
+    for (int k = 1; k <= 2 * T; ++k) {
+        const int c = (S - k + 2 * NW) % NW;
+        const int up = (S - k - 1 + 2 * NW) % NW;
+        const int dn = (S - k + 1 + 2 * NW) % NW;
+        if (RESID && k >= 2 * T - 1) {
+            const int r = i - k - 2 * T;  // row index relative to the first output row
+            float d = 0.0f;
+            half_sweep<Qp, true>(win[c], win[up], win[dn], d);
+            if (lane_out && r >= 0 && r < hs) dmax = fmaxf(dmax, d);
+        } else {
+            float d = 0.0f;
+            half_sweep<Qp, false>(win[c], win[up], win[dn], d);
+        }
+    }
+    const int ro = i - 4 * T;  // output row (relative) finalised by this step
+    if (lane_out && ro >= 0 && ro < hs) {
+        constexpr int so = (S - 2 * T + 2 * NW) % NW;
+        *reinterpret_cast<float4*>(out_row0 + (int64_t)ro * P) = win[so];
+    }
+}
+
+// Per-warp streaming state of k_rb_tblock.
+struct Strip {
+    float* ring;
+    uint64_t* bars;
+    const CUtensorMap* tmap;
+    float* out_row0;
+    int64_t P;
+    int nrows, nchunks, hs, xb, ystart, b, lane;
+    bool lane_out;
+    float dmax;
+};
+
+// Steps S, S+1, ..., NW-1 of one unrolled block of the row loop (S is a template
+// parameter so that every window slot index is a compile-time constant).
+template <int T, int QOFF, bool RESID, int S>
+__device__ __forceinline__ void block_steps(float4 (&win)[2 * T + 2], int ib, Strip& st) {
+    const int i = ib + S;
+    if (i < st.nrows) {
+        const int c = i / kRingRows, rr = i - c * kRingRows, sg = c % kStages;
+        if (rr == 0) mbar_wait(&st.bars[sg], (c / kStages) & 1);
+        win[S] = reinterpret_cast<const float4*>(st.ring + (sg * kRingRows + rr) * kStripW)[st.lane];
+        wave_step<T, QOFF, RESID, S>(win, i, st.hs, st.lane_out, st.out_row0, st.P, st.dmax);
+        if (rr == kRingRows - 1 && c + kStages < st.nchunks) {
+            __syncwarp();  // every lane has consumed stage sg (its values are in registers)
+            if (st.lane == 0) {
+                mbar_expect_tx(&st.bars[sg], kRingRows * kStripW * 4);
+                tma_load_3d(st.ring + sg * kRingRows * kStripW, st.tmap, st.xb, st.ystart + (c + kStages) * kRingRows,
+                            st.b, &st.bars[sg]);
+            }
+        }
+    }
+    if constexpr (S + 1 < 2 * T + 2) block_steps<T, QOFF, RESID, S + 1>(win, ib, st);
+}
+
+template <int T, int QOFF, bool RESID>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1, RelaxArgs a) {
+    constexpr int NW = 2 * T + 2;
+    constexpr int HX = halo_cols(T);
+    constexpr int WOUT = out_cols(T);
+    const int b = blockIdx.y;
+    if (a.done != nullptr && a.done[b]) return;  // scenario converged: whole CTA exits
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nseg = a.seg_end - a.seg_begin;
+    const int task = blockIdx.x * kWarpsPerCta + warp;
+    if (task >= a.n_strips * nseg) return;  // warp-local from here on (no CTA barriers)
+    const int strip = task % a.n_strips;
+    const int seg = a.seg_begin + task / a.n_strips;
+
+    Strip st;
+    st.xb = strip * WOUT - HX;  // first (halo) column of the strip, even
+    const int y0 = seg * a.hseg;  // first output row, even
+    st.hs = min(a.hseg, a.H - y0);
+    st.ystart = y0 - 2 * T;
+    st.nrows = st.hs + 4 * T;
+    st.nchunks = (st.nrows + kRingRows - 1) / kRingRows;
+    st.b = b;
+    st.lane = lane;
+    const int src = a.cur[b] ^ a.lp;  // buffer read by this launch; the other one is written
+    st.tmap = src ? &tmap1 : &tmap0;
+    st.P = a.P;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    st.ring = reinterpret_cast<float*>(smem + warp * kRingBytesPerWarp);
+    st.bars = reinterpret_cast<uint64_t*>(smem + kWarpsPerCta * kRingBytesPerWarp) + warp * kStages;
+
+    if (lane == 0) {
+        prefetch_tmap(st.tmap);
+        for (int s = 0; s < kStages; ++s) mbar_init(&st.bars[s], 1);
+        fence_mbar_init();
+        for (int c = 0; c < kStages && c < st.nchunks; ++c) {
+            mbar_expect_tx(&st.bars[c], kRingRows * kStripW * 4);
+            tma_load_3d(st.ring + c * kRingRows * kStripW, st.tmap, st.xb, st.ystart + c * kRingRows, b, &st.bars[c]);
+        }
+    }
+    __syncwarp();
+
+    const int x = st.xb + 4 * lane;
+    st.lane_out = lane >= HX / 4 && lane < 32 - HX / 4 && x < a.W;
+    st.out_row0 = (src ? a.u0 : a.u1) + (int64_t)b * a.sstride + (int64_t)y0 * a.P + x;
+    st.dmax = 0.0f;
+    float4 win[NW];
+#pragma unroll
+    for (int s = 0; s < NW; ++s) win[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    for (int ib = 0; ib < st.nrows; ib += NW) block_steps<T, QOFF, RESID, 0>(win, ib, st);
+
+    if (RESID) {
+        const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(st.dmax));
+        if (lane == 0 && m != 0u) atomicMax(&a.res[b], m);
+    }
+}
+
+// ---------------------------------------------------------------- bring-up kernel
+// One half-sweep (colour `color`) over the whole grid, in place (same-colour cells
+// never neighbour each other, so the pass is order-free).  Bit-identical to the
+// tile kernel and the oracle; used by the invariance tests.
+__global__ void k_rb_simple(float* __restrict__ u, int64_t P, int64_t sstride, int W, int H, int color, int row_off,
+                            const int* __restrict__ done, unsigned* __restrict__ res) {
+    const int b = blockIdx.z;
+    if (done != nullptr && done[b]) return;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    float* f = u + (int64_t)b * sstride;
+    float d = 0.0f;
+    if (x < W && y < H && ((x + y + row_off) & 1) == color) {
+        const float c = f[(int64_t)y * P + x];
+        if (is_free(c)) {
+            const float e = x + 1 < W ? fabsf(f[(int64_t)y * P + x + 1]) : 0.0f;
+            const float w = x > 0 ? fabsf(f[(int64_t)y * P + x - 1]) : 0.0f;
+            const float n = y > 0 ? fabsf(f[(int64_t)(y - 1) * P + x]) : 0.0f;
+            const float s = y + 1 < H ? fabsf(f[(int64_t)(y + 1) * P + x]) : 0.0f;
+            const float nv = 0.25f * ((e + w) + (n + s));
+            d = fabsf(-nv - c);
+            f[(int64_t)y * P + x] = -nv;
+        }
+    }
+    if (res != nullptr) {
+        const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(d));
+        if ((threadIdx.x & 31) == 0 && m != 0u) atomicMax(&res[b], m);
+    }
+}
+
+// ---------------------------------------------------------------- convergence control (a6)
+// After a chunk of `chunk` sweeps whose last launch accumulated the residual:
+// sweeps += chunk; stop when (sweeps % check_every == 0 && res < tol) or
+// sweeps == max_sweeps (C6).  `where` records which ping-pong buffer
+// holds the scenario's field at the time it finished.
+__global__ void k_check(int B, int* __restrict__ done, int* __restrict__ sweeps, unsigned* __restrict__ res_bits,
+                        float* __restrict__ res_final, int* __restrict__ where, int chunk, int check_every,
+                        int max_sweeps, float tol, const int* __restrict__ cur, int lp) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B || done[b]) return;
+    const int s = sweeps[b] + chunk;
+    sweeps[b] = s;
+    const float r = __uint_as_float(res_bits[b]);
+    res_final[b] = r;
+    res_bits[b] = 0u;
+    where[b] = cur[b] ^ lp;
+    if ((s % check_every == 0 && r < tol) || s >= max_sweeps) done[b] = 1;
+}
+
+// Scenarios that stopped early hold their field in buffer where[b]; move it to the buffer
+// cur[b] ^ lp that the host assumes after the call.
+__global__ void k_fixup(float* __restrict__ u0, float* __restrict__ u1, int64_t sstride, const int* __restrict__ where,
+                        const int* __restrict__ cur, int lp) {
+    const int b = blockIdx.y;
+    const int tgt = cur[b] ^ lp;
+    if (where[b] == tgt) return;
+    const float4* src = reinterpret_cast<const float4*>((tgt ? u0 : u1) + (int64_t)b * sstride);
+    float4* dst = reinterpret_cast<float4*>((tgt ? u1 : u0) + (int64_t)b * sstride);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < sstride / 4; q += (int64_t)gridDim.x * blockDim.x)
+        dst[q] = src[q];
+}
+
+// ---------------------------------------------------------------- host launchers
+template <int T, int QOFF, bool RESID>
+static cudaError_t launch_T(const CUtensorMap& m0, const CUtensorMap& m1, const RelaxArgs& a, int B, cudaStream_t st) {
+    const int nseg = a.seg_end - a.seg_begin;
+    const int tasks = a.n_strips * nseg;
+    dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta, B);
+    const size_t smem = kWarpsPerCta * kRingBytesPerWarp + kWarpsPerCta * kStages * sizeof(uint64_t);
+    k_rb_tblock<T, QOFF, RESID><<<grid, kWarpsPerCta * 32, smem, st>>>(m0, m1, a);
+    return cudaGetLastError();
+}
+
+template <int T>
+static cudaError_t launch_T3(const CUtensorMap& m0, const CUtensorMap& m1, const RelaxArgs& a, int B, int qoff, bool resid,
+                             cudaStream_t st) {
+    if (qoff) return resid ? launch_T<T, 1, true>(m0, m1, a, B, st) : launch_T<T, 1, false>(m0, m1, a, B, st);
+    return resid ? launch_T<T, 0, true>(m0, m1, a, B, st) : launch_T<T, 0, false>(m0, m1, a, B, st);
+}
+
+cudaError_t launch_rb_tblock(int T, const CUtensorMap& m0, const CUtensorMap& m1, const RelaxArgs& a, int B, int qoff,
+                             bool resid, cudaStream_t st) {
+    switch (T) {
+        case 1: return launch_T3<1>(m0, m1, a, B, qoff, resid, st);
+        case 2: return launch_T3<2>(m0, m1, a, B, qoff, resid, st);
+        case 3: return launch_T3<3>(m0, m1, a, B, qoff, resid, st);
+        case 4: return launch_T3<4>(m0, m1, a, B, qoff, resid, st);
+        case 5: return launch_T3<5>(m0, m1, a, B, qoff, resid, st);
+        case 6: return launch_T3<6>(m0, m1, a, B, qoff, resid, st);
+        case 7: return launch_T3<7>(m0, m1, a, B, qoff, resid, st);
+        case 8: return launch_T3<8>(m0, m1, a, B, qoff, resid, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_rb_simple(float* u, int64_t P, int64_t sstride, int W, int H, int B, int color, int row_off,
+                             const int* done, unsigned* res, cudaStream_t st) {
+    dim3 blk(32, 8);
+    dim3 grid((W + 31) / 32, (H + 7) / 8, B);
+    k_rb_simple<<<grid, blk, 0, st>>>(u, P, sstride, W, H, color, row_off, done, res);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check(int B, int* done, int* sweeps, unsigned* res_bits, float* res_final, int* where, int chunk,
+                         int check_every, int max_sweeps, float tol, const int* cur, int lp, cudaStream_t st) {
+    k_check<<<(B + 127) / 128, 128, 0, st>>>(B, done, sweeps, res_bits, res_final, where, chunk, check_every,
+                                             max_sweeps, tol, cur, lp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fixup(float* u0, float* u1, int64_t sstride, int B, const int* where, const int* cur, int lp,
+                         cudaStream_t st) {
+    dim3 grid(256, B);
+    k_fixup<<<grid, 256, 0, st>>>(u0, u1, sstride, where, cur, lp);
+    return cudaGetLastError();
+}
+
+}  // namespace twg

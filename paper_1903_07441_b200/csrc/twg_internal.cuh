@@ -1,0 +1,174 @@
+// twg_internal.cuh -- context layout, kernel argument structs and sm_100a PTX helpers
+// shared by the libtwg.so translation units (product path only; the CPU
+// oracle under oracle/ shares nothing with this file).
+#pragma once
+
+#include <cuda.h>  // CUtensorMap (driver types only; the encode entry point is fetched at runtime)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/twg.h"
+
+namespace twg {
+
+// ---------------------------------------------------------------- relaxation tiling
+// One warp owns a vertical strip of kStripW = 128 cells (4 per lane, one float4)
+// and `hseg` output rows.  Rows stream through a per-warp TMA ring of kStages
+// stages of kRingRows rows; the 2T half-sweeps of T red-black sweeps run as a
+// register wavefront.
+constexpr int kWarpsPerCta = 4;
+constexpr int kStripW = 128;
+constexpr int kRingRows = 4;
+constexpr int kStages = 4;
+constexpr int kRingBytesPerWarp = kStages * kRingRows * kStripW * 4;
+constexpr int kMaxT = 8;
+
+__host__ __device__ constexpr int halo_cols(int T) { return 4 * ((2 * T + 3) / 4); }  // round_up(2T, 4)
+__host__ __device__ constexpr int out_cols(int T) { return kStripW - 2 * halo_cols(T); }
+
+struct RelaxArgs {
+    float* u0;           // ping-pong buffer 0, scenario 0
+    float* u1;           // ping-pong buffer 1, scenario 0
+    const int* cur;      // per-scenario buffer index holding the field at twg_relax entry
+    int lp;              // launch parity: this launch reads buffer cur[b] ^ lp, writes the other
+    int64_t P;           // pitch (floats)
+    int64_t sstride;     // scenario stride (floats)
+    int W, H;
+    int n_strips, hseg;
+    int seg_begin, seg_end;  // launched segment range
+    const int* done;     // per-scenario done flags
+    unsigned* res;       // per-scenario residual (float bits, atomicMax), used when RESID
+};
+
+// Per-scenario parameters of one encode (rows a1-a3), built on the host.
+struct ScenParams {
+    double xr, yr, c, s, speed;  // robot position, cos/sin(theta) (host libm), speed
+    int b;                       // scenario index
+    int gx, gy;                  // goal cell
+    int rcx, rcy;                // robot cell
+    int old_gx, old_gy;          // previous goal (-1: none)
+    int warm;
+    int cur;                     // buffer index holding the scenario's field
+    int n_tracks;
+    int n_prev_boxes;
+};
+
+struct WarpCfgDev {
+    double dt, Q[16], w, eps_v, rs;
+    int hmax;
+};
+
+struct PathMeta {  // per scenario, written by k_walk / k_band
+    int n_cells;
+    int status;
+    int n_smooth;
+    float next_x, next_y;
+    int pad[3];
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TWG_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TWG_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 3D TMA tile load (global -> shared), completion signalled on `bar` (complete_tx).
+// Out-of-bounds elements (negative or >= extent coordinates) are zero-filled,
+// i.e. +0.0f = fixed obstacle, which is the grid-boundary condition (C4).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// Field encoding (include/twg.h): free = sign bit set (value -u), fixed = sign clear.
+__device__ __forceinline__ bool is_free(float v) { return __float_as_int(v) < 0; }
+
+}  // namespace twg
+
+// ---------------------------------------------------------------- context
+struct twg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int W = 0, H = 0, B = 0, row_off = 0;
+    double cs = 0.1, ox = 0.0, oy = 0.0;
+    int64_t P = 0;        // pitch in floats
+    int64_t sstride = 0;  // floats per scenario field
+    float* u[2] = {nullptr, nullptr};
+    std::vector<int> cur;          // per scenario: which buffer holds the current field
+    int* d_cur = nullptr;          // device copy used by the tile kernel
+    CUtensorMap tmap[2];
+    uint8_t* mask = nullptr;       // device [B][H][W]
+    std::vector<uint8_t> hmask;    // host copy (validation only)
+    // relaxation control, [B] each
+    int* d_done = nullptr;
+    int* d_sweeps = nullptr;
+    unsigned* d_res_bits = nullptr;
+    float* d_res = nullptr;
+    int* d_where = nullptr;
+    int* d_flags = nullptr;
+    // encode state
+    struct Scen {
+        int gx = -1, gy = -1, rcx = -1, rcy = -1;
+        int n_tracks = 0, n_boxes = 0;
+        bool encoded = false, static_dirty = true;
+    };
+    std::vector<Scen> scen;
+    int track_cap = 0;                 // per scenario
+    twg_track* d_tracks = nullptr;     // [B][cap]
+    int* d_t = nullptr;                // [B][cap]
+    int* d_j = nullptr;
+    double* d_pred = nullptr;          // [B][cap][3]
+    int4* d_boxes = nullptr;           // [B][cap] (x0, x1, y0, y1) inclusive; empty if x0 > x1
+    twg::ScenParams* d_params = nullptr;
+    int params_cap = 0;
+    twg::WarpCfgDev* d_wcfg = nullptr;
+    int* d_track_off = nullptr;        // scatter offsets for device-side track input
+    int track_off_cap = 0;
+    // path buffers
+    int path_len_cap = 0, smooth_cap = 0;
+    int2* d_cells = nullptr;           // [B][path_len_cap]
+    float2* d_wp = nullptr;            // [B][path_len_cap]
+    float2* d_smooth = nullptr;        // [B][smooth_cap]
+    twg::PathMeta* d_meta = nullptr;   // [B]
+    // pinned host staging
+    void* h_stage = nullptr;
+    size_t h_stage_bytes = 0;
+    size_t stage_off = 0;
+    // accounting
+    int64_t launches = 0;
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    int ev_used = 0;
+    int64_t prof_launches = 0, prof_cells = 0;
+    double prof_ms = 0.0;
+    std::string err;
+};

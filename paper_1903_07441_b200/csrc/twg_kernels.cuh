@@ -1,0 +1,62 @@
+// twg_kernels.cuh -- host launchers of the libtwg.so kernels (product path).
+#pragma once
+#include "twg_internal.cuh"
+
+namespace twg {
+
+// k_relax.cu (rows a4-a6)
+cudaError_t launch_rb_tblock(int T, const CUtensorMap& map0, const CUtensorMap& map1, const RelaxArgs& a, int B, int qoff, bool resid,
+                             cudaStream_t st);
+cudaError_t launch_rb_simple(float* u, int64_t P, int64_t sstride, int W, int H, int B, int color, int row_off,
+                             const int* done, unsigned* res, cudaStream_t st);
+cudaError_t launch_check(int B, int* done, int* sweeps, unsigned* res_bits, float* res_final, int* where, int chunk,
+                         int check_every, int max_sweeps, float tol, const int* cur, int lp, cudaStream_t st);
+cudaError_t launch_init_field(float* u, int64_t P, int64_t sstride, int W, int H, int B, cudaStream_t st);
+cudaError_t launch_convert(const float* src, int64_t P, int W, int H, float* dst, int mode, cudaStream_t st);
+cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P, cudaStream_t st);
+cudaError_t launch_fixup(float* u0, float* u1, int64_t sstride, int B, const int* where, const int* cur, int lp,
+                         cudaStream_t st);
+
+// k_stamp.cu (rows a1-a3)
+struct EncodeArgs {
+    float* u0;             // ping-pong buffers, scenario 0 (ScenParams::cur selects)
+    float* u1;
+    int64_t P, sstride;
+    int W, H;
+    const uint8_t* mask;   // [B][H][W]
+    const ScenParams* params;  // [nscen]
+    int nscen;
+    const WarpCfgDev* wcfg;
+    const twg_track* tracks;   // [B][cap]
+    int cap;
+    int* t_out;            // [B][cap]
+    int* j_out;
+    double* pred;          // [B][cap][3]
+    int4* boxes;           // [B][cap]
+    int* flags;            // [B] warning flags
+    double cs, ox, oy;
+};
+cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_tracks, int any_cold, int* n_launch,
+                          cudaStream_t st);
+cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nscen, const int* scen_b, twg_track* dst,
+                                  int cap, cudaStream_t st);
+
+// k_path.cu (rows a7-a9)
+struct PathArgs {
+    const float* u0;       // ping-pong buffers, scenario 0 (ScenParams::cur selects)
+    const float* u1;
+    int64_t P, sstride;
+    int W, H;
+    const ScenParams* params;  // robot/goal cells per entry
+    int nscen;
+    int max_len, max_smooth, iters;
+    float step, kt;
+    int2* cells;           // [B][max_len_cap]
+    float2* wp;            // [B][max_len_cap]
+    float2* smooth;        // [B][smooth_cap]
+    int len_cap, smooth_cap;
+    PathMeta* meta;        // [B]
+};
+cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
+
+}  // namespace twg

@@ -1,0 +1,257 @@
+"""Thin ctypes binding of include/twg.h (argument marshalling only).
+
+Every function below forwards to the C ABI of ``libtwg.so`` with the same name;
+every step of the hot path runs in the library's sm_100a kernels.  Arrays may
+be numpy arrays (host) or torch CUDA tensors (device); PyTorch is used only
+for device memory and streams.  There is no CPU fallback: if the library is
+missing or fails to load, :func:`lib` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtwg.so")
+
+OK, W_GOAL_SWALLOWED, W_TRUNCATED = 0, 1, 2
+E_INVALID_ARG, E_OUT_OF_BOUNDS, E_OVERLAPPING_CLASSES, E_INVALID_START = -1, -2, -3, -4
+E_NO_PATH, E_CUDA, E_NCCL, E_NO_MEMORY = -5, -6, -7, -8
+
+
+class GridDesc(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("batch", C.c_int32), ("row_offset", C.c_int32),
+                ("cell_size", C.c_double), ("origin_x", C.c_double), ("origin_y", C.c_double)]
+
+
+class Robot(C.Structure):
+    _fields_ = [("x", C.c_double), ("y", C.c_double), ("theta", C.c_double), ("speed", C.c_double)]
+
+
+class Track(C.Structure):
+    _fields_ = [("x", C.c_double * 4), ("P", C.c_double * 16)]
+
+
+class WarpCfg(C.Structure):
+    _fields_ = [("dt", C.c_double), ("Q", C.c_double * 16), ("warp_spacing", C.c_double), ("eps_v", C.c_double),
+                ("safety_radius", C.c_double), ("horizon_max", C.c_int32), ("reserved", C.c_int32)]
+
+
+class RelaxCfg(C.Structure):
+    _fields_ = [("max_sweeps", C.c_int32), ("check_every", C.c_int32), ("warm_start", C.c_int32),
+                ("temporal_depth", C.c_int32), ("tol", C.c_float), ("rows_per_warp", C.c_int32),
+                ("sync_every", C.c_int32), ("reserved", C.c_int32)]
+
+
+class BandCfg(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("max_len", C.c_int32), ("max_smooth", C.c_int32),
+                ("reserved", C.c_int32), ("step", C.c_float), ("k_t", C.c_float)]
+
+
+class PlanResult(C.Structure):
+    _fields_ = [("status", C.c_int32), ("sweeps", C.c_int32), ("n_cells", C.c_int32), ("n_smooth", C.c_int32),
+                ("residual", C.c_float), ("next_x", C.c_float), ("next_y", C.c_float), ("walk_status", C.c_int32)]
+
+
+# (name, restype, argtypes) for every symbol of include/twg.h
+_P = C.c_void_p
+SIGNATURES = [
+    ("twg_create", C.c_int32, [C.POINTER(GridDesc), C.c_int32, _P, C.POINTER(_P)]),
+    ("twg_destroy", C.c_int32, [_P]),
+    ("twg_set_static", C.c_int32, [_P, C.c_int32, _P]),
+    ("twg_set_obstacles", C.c_int32, [_P, C.c_int32, C.POINTER(Robot), C.c_int32, C.c_int32, _P, C.c_int32,
+                                      C.POINTER(WarpCfg), C.c_int32]),
+    ("twg_relax", C.c_int32, [_P, C.POINTER(RelaxCfg), _P, _P]),
+    ("twg_extract_path", C.c_int32, [_P, C.c_int32, C.POINTER(BandCfg), _P, _P, _P, _P, _P]),
+    ("twg_plan_step", C.c_int32, [_P, C.c_int32, _P, _P, _P, _P, C.POINTER(WarpCfg), C.POINTER(RelaxCfg),
+                                  C.POINTER(BandCfg), _P, _P, _P]),
+    ("twg_get_field", C.c_int32, [_P, C.c_int32, _P, C.c_int32]),
+    ("twg_set_field", C.c_int32, [_P, C.c_int32, _P]),
+    ("twg_get_warp", C.c_int32, [_P, C.c_int32, C.c_int32, _P, _P, _P]),
+    ("twg_field_ptr", C.c_int32, [_P, C.c_int32, C.POINTER(_P), C.POINTER(C.c_int64)]),
+    ("twg_kernel_launches", C.c_int64, [_P]),
+    ("twg_profile", C.c_int32, [_P, C.c_int32]),
+    ("twg_profile_read", C.c_int32, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("twg_last_error", C.c_char_p, [_P]),
+]
+
+_lib = None
+
+
+def lib():
+    """Load libtwg.so (raises if it is missing: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class TwgError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"twg status {status}: {msg}")
+        self.status = status
+
+
+def _ptr(a):
+    """Raw address of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags.c_contiguous
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        assert a.is_contiguous()
+        return a.data_ptr()
+    raise TypeError(type(a))
+
+
+def _check(ctx, st, ok=(OK, W_GOAL_SWALLOWED, W_TRUNCATED)):
+    if st not in ok:
+        raise TwgError(st, lib().twg_last_error(ctx).decode())
+    return st
+
+
+def warp_cfg(dt=0.1, Q=None, warp_spacing=1.0, eps_v=0.05, safety_radius=0.5, horizon_max=20):
+    c = WarpCfg()
+    c.dt = dt
+    q = np.zeros(16) if Q is None else np.asarray(Q, np.float64).reshape(16)
+    if Q is None:
+        q[0] = q[5] = 1e-3 * dt ** 4 / 4.0
+        q[10] = q[15] = 1e-3 * dt ** 2
+    for k in range(16):
+        c.Q[k] = float(q[k])
+    c.warp_spacing, c.eps_v, c.safety_radius, c.horizon_max = warp_spacing, eps_v, safety_radius, horizon_max
+    return c
+
+
+def relax_cfg(max_sweeps=100, check_every=0, warm_start=1, temporal_depth=0, tol=0.0, rows_per_warp=0,
+              sync_every=0):
+    return RelaxCfg(max_sweeps, check_every, warm_start, temporal_depth, tol, rows_per_warp, sync_every, 0)
+
+
+def band_cfg(iterations=50, max_len=4096, max_smooth=8192, step=0.25, k_t=1.0):
+    return BandCfg(iterations, max_len, max_smooth, 0, step, k_t)
+
+
+def tracks_array(tracks):
+    """float64 [n, 20] (x[4], P[16]) -> contiguous array with the twg_track layout."""
+    t = np.ascontiguousarray(np.asarray(tracks, np.float64).reshape(-1, 20))
+    return t
+
+
+class Planner:
+    """Owns one twg_ctx.  Method names mirror the C ABI (twg_<name>)."""
+
+    def __init__(self, width, height, batch=1, cell_size=0.1, origin=(0.0, 0.0), device=0, stream=None,
+                 row_offset=0):
+        self.W, self.H, self.B = int(width), int(height), int(batch)
+        d = GridDesc(self.W, self.H, self.B, int(row_offset), float(cell_size), float(origin[0]), float(origin[1]))
+        h = C.c_void_p()
+        st = lib().twg_create(C.byref(d), int(device), stream, C.byref(h))
+        if st != OK:
+            raise TwgError(st, lib().twg_last_error(None).decode())
+        self.ctx = h
+
+    def close(self):
+        if self.ctx:
+            lib().twg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- a1-a3
+    def set_static(self, occ, b=-1):
+        return _check(self.ctx, lib().twg_set_static(self.ctx, b, _ptr(occ)))
+
+    def set_obstacles(self, b, robot, goal, tracks, cfg, warm=0):
+        t = tracks if hasattr(tracks, "data_ptr") else tracks_array(tracks)
+        n = int(t.shape[0])
+        r = Robot(*[float(v) for v in robot])
+        return _check(self.ctx, lib().twg_set_obstacles(self.ctx, b, C.byref(r), int(goal[0]), int(goal[1]),
+                                                        _ptr(t) if n else None, n, C.byref(cfg), int(warm)))
+
+    # -- a4-a6
+    def relax(self, cfg, want_result=True):
+        if not want_result:
+            _check(self.ctx, lib().twg_relax(self.ctx, C.byref(cfg), None, None))
+            return None, None
+        sw = np.zeros(self.B, np.int32)
+        res = np.zeros(self.B, np.float32)
+        _check(self.ctx, lib().twg_relax(self.ctx, C.byref(cfg), _ptr(sw), _ptr(res)))
+        return sw, res
+
+    # -- a7-a9
+    def extract_path(self, b, cfg):
+        cells = np.zeros((cfg.max_len, 2), np.int32)
+        sm = np.zeros((cfg.max_smooth, 2), np.float32)
+        nc = C.c_int32()
+        ns = C.c_int32()
+        nxt = np.zeros(2, np.float32)
+        st = lib().twg_extract_path(self.ctx, b, C.byref(cfg), _ptr(cells), C.byref(nc), _ptr(sm), C.byref(ns),
+                                    _ptr(nxt))
+        _check(self.ctx, st, ok=(OK, W_TRUNCATED, E_NO_PATH))
+        return st, cells[: nc.value].copy(), sm[: min(ns.value, cfg.max_smooth)].copy(), ns.value, (float(nxt[0]), float(nxt[1]))
+
+    def plan_step(self, b, robots, goals, tracks, n_tracks, wcfg, rcfg, bcfg, want_paths=True):
+        """b >= 0: one scenario; b = -1: all.  tracks: concatenated [sum n, 20] (numpy or CUDA tensor)."""
+        nb = 1 if b >= 0 else self.B
+        rob = (Robot * nb)(*[Robot(*[float(v) for v in r]) for r in robots])
+        g = np.ascontiguousarray(np.asarray(goals, np.int32).reshape(nb, 2))
+        nt = np.ascontiguousarray(np.asarray(n_tracks, np.int32).reshape(nb))
+        t = tracks if hasattr(tracks, "data_ptr") else tracks_array(tracks)
+        out = (PlanResult * nb)()
+        cells = np.zeros((nb, bcfg.max_len, 2), np.int32) if want_paths else None
+        sm = np.zeros((nb, bcfg.max_smooth, 2), np.float32) if want_paths else None
+        st = lib().twg_plan_step(self.ctx, b, rob, _ptr(g), _ptr(t) if int(nt.sum()) else None, _ptr(nt),
+                                 C.byref(wcfg), C.byref(rcfg), C.byref(bcfg), out, _ptr(cells), _ptr(sm))
+        _check(self.ctx, st, ok=(OK, W_GOAL_SWALLOWED, W_TRUNCATED, E_NO_PATH))
+        return st, list(out), cells, sm
+
+    # -- field access
+    def get_field(self, b=0, mode=1, out=None):
+        if out is None:
+            out = np.zeros((self.H, self.W), np.float32)
+        _check(self.ctx, lib().twg_get_field(self.ctx, b, _ptr(out), int(mode)))
+        return out
+
+    def set_field(self, raw, b=0):
+        return _check(self.ctx, lib().twg_set_field(self.ctx, b, _ptr(raw)))
+
+    def get_warp(self, b, n):
+        t = np.zeros(max(n, 1), np.int32)
+        j = np.zeros(max(n, 1), np.int32)
+        pred = np.zeros((max(n, 1), 3))
+        _check(self.ctx, lib().twg_get_warp(self.ctx, b, n, _ptr(t), _ptr(j), _ptr(pred)))
+        return t[:n], j[:n], pred[:n]
+
+    def field_ptr(self, b=0):
+        p = C.c_void_p()
+        pitch = C.c_int64()
+        _check(self.ctx, lib().twg_field_ptr(self.ctx, b, C.byref(p), C.byref(pitch)))
+        return p.value, pitch.value
+
+    def kernel_launches(self):
+        return int(lib().twg_kernel_launches(self.ctx))
+
+    def profile(self, enable):
+        return _check(self.ctx, lib().twg_profile(self.ctx, int(enable)))
+
+    def profile_read(self):
+        ms = C.c_double()
+        nl = C.c_int64()
+        cells = C.c_int64()
+        _check(self.ctx, lib().twg_profile_read(self.ctx, C.byref(ms), C.byref(nl), C.byref(cells)))
+        return ms.value, nl.value, cells.value
