@@ -168,8 +168,9 @@ TWG_API twg_status twg_set_static(twg_ctx* ctx, int32_t b, const uint8_t* occ);
  *      position become obstacles, static walls stay obstacles, the goal cell
  *      is the goal, the robot's cell stays free (C22).
  * warm = 0: every free cell restarts at 0.5 ("cleared");
- * warm = 1: free cells keep their value, cells fixed in the previous call
- * and free now restart at 0.5 (C7).
+ * warm = 1: every free cell keeps the value it holds, including cells fixed
+ * in the previous call and free now (a released obstacle keeps u = 0, a
+ * released goal u = 1) ("the values evolve slowly"; C7).
  * tracks: n entries, host or device pointer (n may be 0).
  * Returns OK, W_GOAL_SWALLOWED, or OUT_OF_BOUNDS / OVERLAPPING_CLASSES /
  * INVALID_START / INVALID_ARG (validated before any device work). */

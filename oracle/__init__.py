@@ -68,7 +68,7 @@ def lib():
         L.orc_classify.argtypes = [i32, i32, d, d, d, P, i32, i32, d, d, d, d, i32, P,
                                    d, P, d, d, d, i32, P, P, P, P]
         L.orc_init_u32.restype = None
-        L.orc_init_u32.argtypes = [i64, P, P, P, P]
+        L.orc_init_u32.argtypes = [i64, P, P, P]
         L.orc_init_u64.restype = None
         L.orc_init_u64.argtypes = [i64, P, P]
         L.orc_relax_f32.restype = i32
@@ -163,15 +163,15 @@ def robot_cell(scene):
             int(math.floor((yr - scene.origin[1]) / scene.cell_size)))
 
 
-def init_u32(cls, cls_prev=None, u_prev=None):
+def init_u32(cls, u_prev=None):
+    """cold (u_prev None): goal 1, obstacle 0, free 0.5; warm: free cells keep u_prev (C7)."""
     cls = np.ascontiguousarray(cls, np.uint8)
     u = np.zeros(cls.shape, np.float32)
-    if cls_prev is None:
-        lib().orc_init_u32(cls.size, _p(cls), None, None, _p(u))
+    if u_prev is None:
+        lib().orc_init_u32(cls.size, _p(cls), None, _p(u))
     else:
-        cp = np.ascontiguousarray(cls_prev, np.uint8)
         up = np.ascontiguousarray(u_prev, np.float32)
-        lib().orc_init_u32(cls.size, _p(cls), _p(cp), _p(up), _p(u))
+        lib().orc_init_u32(cls.size, _p(cls), _p(up), _p(u))
     return u
 
 
@@ -273,7 +273,7 @@ def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0
     if prev is None:
         u = init_u32(cls)
     else:
-        u = init_u32(cls, prev["cls"], prev["u"])
+        u = init_u32(cls, prev["u"])
     sweeps, res = relax_f32(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol)
     if max_len is None:
         max_len = 4 * (scene.W + scene.H)

@@ -241,17 +241,17 @@ int32_t orc_classify(int32_t W, int32_t H, double cs, double ox, double oy,
 }
 
 /* Field initialisation in u-space (C7).
- * cold (cls_prev == NULL): goal 1, obstacle 0, free 0.5 ("initialized with 0.5").
- * warm: fixed-now cells take their fixed value; cells fixed in the previous
- * tick and free now restart at 0.5; other free cells keep u_prev
- * ("the values evolve slowly anyways"). */
-void orc_init_u32(int64_t ncell, const uint8_t* cls, const uint8_t* cls_prev,
-                  const float* u_prev, float* u)
+ * cold (u_prev == NULL): goal 1, obstacle 0, free 0.5 ("initialized with 0.5").
+ * warm: fixed-now cells take their fixed value; every free cell keeps the value
+ * it held after the previous tick, including cells that were fixed then (an
+ * obstacle cell released keeps u = 0, i.e. phi = 1) ("the values
+ * evolve slowly anyways"). */
+void orc_init_u32(int64_t ncell, const uint8_t* cls, const float* u_prev, float* u)
 {
     for (int64_t q = 0; q < ncell; ++q) {
         if (cls[q] == ORC_GOAL) u[q] = 1.0f;
         else if (cls[q] == ORC_OBSTACLE) u[q] = 0.0f;
-        else if (cls_prev == NULL || cls_prev[q] != ORC_FREE) u[q] = 0.5f;
+        else if (u_prev == NULL) u[q] = 0.5f;
         else u[q] = u_prev[q];
     }
 }

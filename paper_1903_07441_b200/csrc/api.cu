@@ -503,6 +503,8 @@ twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg)
     p.len_cap = c->path_len_cap;
     p.smooth_cap = c->smooth_cap;
     p.meta = c->d_meta;
+    p.idx = c->d_idx;
+    p.istride = c->sstride;
     int nl = 0;
     TWG_CUDA(c, launch_path(p, &nl, c->stream));
     c->launches += nl;
@@ -557,6 +559,7 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     CK(dev_alloc(&c->d_cur, B));
     CK(dev_alloc(&c->d_flags, B));
     CK(dev_alloc(&c->d_meta, B));
+    CK(dev_alloc(&c->d_idx, cells));
     CK(dev_alloc(&c->d_wcfg, 1));
     CK(cudaMemsetAsync(c->mask, 0, B * c->H * c->W, c->stream));
     CK(cudaMemsetAsync(c->d_meta, 0, B * sizeof(PathMeta), c->stream));
@@ -580,7 +583,7 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
     void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_done,  c->d_sweeps, c->d_res_bits, c->d_res,
                     c->d_where,  c->d_cur,     c->d_flags, c->d_meta,  c->d_wcfg,   c->d_tracks,   c->d_t,
                     c->d_j,      c->d_pred,    c->d_boxes, c->d_params, c->d_track_off, c->d_cells, c->d_wp,
-                    c->d_smooth};
+                    c->d_smooth, c->d_idx};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);

@@ -2,8 +2,9 @@
 // P:679-691).
 //
 //   k_encode_cold     cold encode: free 0.5, static walls +0.0
-//   k_unstamp         warm encode: cells fixed by last tick's stamps and free now -> 0.5 (C7)
-//   k_goal_reset      warm encode: the previous goal cell -> 0.5 when the goal moved (C7)
+//   k_unstamp         warm encode: cells stamped last tick are released as free cells that keep
+//                     their value u = 0 (C7: warm start keeps every value)
+//   k_goal_reset      warm encode: the previous goal cell is released as a free cell keeping u = 1
 //   k_track_predict   one thread per track, fp64: warp radius (Eq. 15 closed form, C16),
 //                     warp number t (C17), horizon j (Eq. 16, C18), j Kalman predicts
 //                     (Eqs. 9-10), footprint R^2 (C19-C20), bounding box
@@ -42,7 +43,7 @@ __global__ void k_unstamp(EncodeArgs e) {
     for (int q = threadIdx.x; q < n; q += blockDim.x) {
         const int x = bx.x + q % nx, y = bx.z + q / nx;
         float* p = f + (int64_t)y * e.P + x;
-        if (__float_as_uint(*p) == 0u && m[(int64_t)y * e.W + x] == 0) *p = -0.5f;
+        if (__float_as_uint(*p) == 0u && m[(int64_t)y * e.W + x] == 0) *p = -0.0f;  // free, u = 0
     }
 }
 
@@ -54,7 +55,7 @@ __global__ void k_goal_reset(EncodeArgs e) {
     if (sp.old_gx == sp.gx && sp.old_gy == sp.gy) return;
     const int b = sp.b;
     if (e.mask[((int64_t)b * e.H + sp.old_gy) * e.W + sp.old_gx]) return;
-    (sp.cur ? e.u1 : e.u0)[(int64_t)b * e.sstride + (int64_t)sp.old_gy * e.P + sp.old_gx] = -0.5f;
+    (sp.cur ? e.u1 : e.u0)[(int64_t)b * e.sstride + (int64_t)sp.old_gy * e.P + sp.old_gx] = -1.0f;  // free, u = 1
 }
 
 // Round half away from zero of a non-negative double (C25; equals llround for x >= 0).

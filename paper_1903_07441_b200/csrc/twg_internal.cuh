@@ -159,6 +159,7 @@ struct twg_ctx {
     float2* d_wp = nullptr;            // [B][path_len_cap]
     float2* d_smooth = nullptr;        // [B][smooth_cap]
     twg::PathMeta* d_meta = nullptr;   // [B]
+    uint8_t* d_idx = nullptr;          // index matrix [B][H][P] bytes
     // pinned host staging
     void* h_stage = nullptr;
     size_t h_stage_bytes = 0;

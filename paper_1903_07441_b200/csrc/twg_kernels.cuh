@@ -56,6 +56,8 @@ struct PathArgs {
     float2* smooth;        // [B][smooth_cap]
     int len_cap, smooth_cap;
     PathMeta* meta;        // [B]
+    uint8_t* idx;          // index matrix M_idx, [B][H][P] bytes (Eq. 3)
+    int64_t istride;       // bytes per scenario (H * P)
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
 
