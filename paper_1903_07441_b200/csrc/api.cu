@@ -54,13 +54,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 3D map {W, H, B} over one ping-pong buffer; box {128, kRingRows, 1}; OOB -> zero fill.
-bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P) {
+// 3D map {W, H, B} over one ping-pong buffer; box {128, rows, 1}; OOB -> zero fill.
+bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P, int rows) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
     cuuint64_t strides[2] = {(cuuint64_t)(P * 4), (cuuint64_t)(P * 4 * (int64_t)H)};
-    cuuint32_t box[3] = {(cuuint32_t)kStripW, (cuuint32_t)kRingRows, 1};
+    cuuint32_t box[3] = {(cuuint32_t)kStripW, (cuuint32_t)rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -333,19 +333,25 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     return TWG_OK;
 }
 
+// Output rows per warp.  hseg + 4T is made a multiple of NW = 2T + 2 (the kernel streams whole
+// NW-row blocks, so any other value pays for padded rows); hseg is even (colour parity of the
+// first row is a compile-time constant).
 int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows) {
+    const int NW = 2 * T + 2;
     int h;
     if (cfg_rows > 0) {
         h = cfg_rows;
     } else {
-        const int target = 148 * 16;  // warps in flight per launch (4 CTAs x 4 warps per SM)
+        const int target = 148 * 16;  // warps per launch (4 CTAs x 4 warps per SM)
         int segs = (target + n_strips * nscen - 1) / (n_strips * nscen);
         segs = std::max(segs, 1);
         h = (H + segs - 1) / segs;
         h = std::max(h, 8 * T);
+        const int k = std::max(1, (h + 4 * T + NW / 2) / NW);
+        h = std::max(k * NW - 4 * T, 2);
     }
     h = std::min(h, H);
-    h = (h + 1) & ~1;  // even (red/black parity of the first row)
+    h = (h + 1) & ~1;
     return std::max(h, 2);
 }
 
@@ -413,7 +419,7 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
                     e1 = c->ev_pool[c->ev_used++];
                     TWG_CUDA(c, cudaEventRecord(e0, c->stream));
                 }
-                TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0], c->tmap[1], a, B, qoff, q + 1 == plan.size(), c->stream));
+                TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0][t], c->tmap[1][t], a, B, qoff, q + 1 == plan.size(), c->stream));
                 if (c->prof) {
                     TWG_CUDA(c, cudaEventRecord(e1, c->stream));
                     c->prof_launches += 1;
@@ -460,8 +466,8 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
 // Rows a7-a9 for a list of scenarios (path kernels only; results stay on device).
 twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg) {
     if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null band cfg");
-    if (cfg->max_len < 1 || cfg->max_smooth < 1 || cfg->iterations < 0)
-        return fail(c, TWG_E_INVALID_ARG, "band cfg: max_len, max_smooth >= 1, iterations >= 0");
+    if (cfg->max_len < 1 || cfg->max_smooth < 1 || cfg->iterations < 0 || cfg->iterations > 6000)
+        return fail(c, TWG_E_INVALID_ARG, "band cfg: max_len, max_smooth >= 1, 0 <= iterations <= 6000");
     twg_status st = ensure_path_cap(c, cfg->max_len, cfg->max_smooth);
     if (st != TWG_OK) return st;
     const int ns = (int)bs.size();
@@ -567,9 +573,10 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     CK(launch_init_field(c->u[1], c->P, c->sstride, c->W, c->H, c->B, c->stream));
     c->launches += 2;
     c->hmask.assign(B * c->H * c->W, 0);
-    if (!make_tmap(&c->tmap[0], c->u[0], c->W, c->H, c->B, c->P) ||
-        !make_tmap(&c->tmap[1], c->u[1], c->W, c->H, c->B, c->P))
-        return bail(TWG_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point unavailable or bad layout)");
+    for (int t = 1; t <= kMaxT; ++t)
+        if (!make_tmap(&c->tmap[0][t], c->u[0], c->W, c->H, c->B, c->P, 2 * t + 2) ||
+            !make_tmap(&c->tmap[1][t], c->u[1], c->W, c->H, c->B, c->P, 2 * t + 2))
+            return bail(TWG_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point unavailable or bad layout)");
     CK(cudaStreamSynchronize(c->stream));
 #undef CK
     *out = c;

@@ -83,43 +83,30 @@ __device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, int h
 
 // Per-warp streaming state of k_rb_tblock.
 struct Strip {
-    float* ring;
-    uint64_t* bars;
-    const CUtensorMap* tmap;
+    const float* rows;  // current ring stage: NW rows x 128 floats
     float* out_row0;
     int64_t P;
-    int nrows, nchunks, hs, xb, ystart, b, lane;
+    int hs, lane;
     bool lane_out;
     float dmax;
 };
 
-// Steps S, S+1, ..., NW-1 of one unrolled block of the row loop (S is a template
-// parameter so that every window slot index is a compile-time constant).
+// Steps S, S+1, ..., NW-1 of one unrolled block of the row loop.  S is a template parameter so
+// that every window slot and every ring offset is a compile-time constant; the block has no
+// per-row branch (the row count is padded to a multiple of NW on the host).
 template <int T, int QOFF, bool RESID, int S>
 __device__ __forceinline__ void block_steps(float4 (&win)[2 * T + 2], int ib, Strip& st) {
-    const int i = ib + S;
-    if (i < st.nrows) {
-        const int c = i / kRingRows, rr = i - c * kRingRows, sg = c % kStages;
-        if (rr == 0) mbar_wait(&st.bars[sg], (c / kStages) & 1);
-        win[S] = reinterpret_cast<const float4*>(st.ring + (sg * kRingRows + rr) * kStripW)[st.lane];
-        wave_step<T, QOFF, RESID, S>(win, i, st.hs, st.lane_out, st.out_row0, st.P, st.dmax);
-        if (rr == kRingRows - 1 && c + kStages < st.nchunks) {
-            __syncwarp();  // every lane has consumed stage sg (its values are in registers)
-            if (st.lane == 0) {
-                mbar_expect_tx(&st.bars[sg], kRingRows * kStripW * 4);
-                tma_load_3d(st.ring + sg * kRingRows * kStripW, st.tmap, st.xb, st.ystart + (c + kStages) * kRingRows,
-                            st.b, &st.bars[sg]);
-            }
-        }
-    }
+    win[S] = reinterpret_cast<const float4*>(st.rows + S * kStripW)[st.lane];
+    wave_step<T, QOFF, RESID, S>(win, ib + S, st.hs, st.lane_out, st.out_row0, st.P, st.dmax);
     if constexpr (S + 1 < 2 * T + 2) block_steps<T, QOFF, RESID, S + 1>(win, ib, st);
 }
 
 template <int T, int QOFF, bool RESID>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1, RelaxArgs a) {
-    constexpr int NW = 2 * T + 2;
+    constexpr int NW = 2 * T + 2;          // rows per TMA box = rows per unrolled block
     constexpr int HX = halo_cols(T);
     constexpr int WOUT = out_cols(T);
+    constexpr int STAGE_F = NW * kStripW;  // floats per ring stage
     const int b = blockIdx.y;
     if (a.done != nullptr && a.done[b]) return;  // scenario converged: whole CTA exits
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -128,36 +115,34 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     if (task >= a.n_strips * nseg) return;  // warp-local from here on (no CTA barriers)
     const int strip = task % a.n_strips;
     const int seg = a.seg_begin + task / a.n_strips;
-
-    Strip st;
-    st.xb = strip * WOUT - HX;  // first (halo) column of the strip, even
-    const int y0 = seg * a.hseg;  // first output row, even
-    st.hs = min(a.hseg, a.H - y0);
-    st.ystart = y0 - 2 * T;
-    st.nrows = st.hs + 4 * T;
-    st.nchunks = (st.nrows + kRingRows - 1) / kRingRows;
-    st.b = b;
-    st.lane = lane;
     const int src = a.cur[b] ^ a.lp;  // buffer read by this launch; the other one is written
-    st.tmap = src ? &tmap1 : &tmap0;
+    const CUtensorMap* tmap = src ? &tmap1 : &tmap0;
+
+    const int xb = strip * WOUT - HX;  // first (halo) column of the strip, even
+    const int y0 = seg * a.hseg;       // first output row, even
+    Strip st;
+    st.hs = min(a.hseg, a.H - y0);
+    const int ystart = y0 - 2 * T;
+    const int nblk = (st.hs + 4 * T + NW - 1) / NW;  // rows ystart .. ystart + nblk*NW - 1
+    st.lane = lane;
     st.P = a.P;
 
     extern __shared__ __align__(128) unsigned char smem[];
-    st.ring = reinterpret_cast<float*>(smem + warp * kRingBytesPerWarp);
-    st.bars = reinterpret_cast<uint64_t*>(smem + kWarpsPerCta * kRingBytesPerWarp) + warp * kStages;
+    float* ring = reinterpret_cast<float*>(smem) + warp * (kStages * STAGE_F);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWarpsPerCta * kStages * STAGE_F * 4) + warp * kStages;
 
     if (lane == 0) {
-        prefetch_tmap(st.tmap);
-        for (int s = 0; s < kStages; ++s) mbar_init(&st.bars[s], 1);
+        prefetch_tmap(tmap);
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
-        for (int c = 0; c < kStages && c < st.nchunks; ++c) {
-            mbar_expect_tx(&st.bars[c], kRingRows * kStripW * 4);
-            tma_load_3d(st.ring + c * kRingRows * kStripW, st.tmap, st.xb, st.ystart + c * kRingRows, b, &st.bars[c]);
+        for (int c = 0; c < kStages && c < nblk; ++c) {
+            mbar_expect_tx(&bars[c], STAGE_F * 4);
+            tma_load_3d(ring + c * STAGE_F, tmap, xb, ystart + c * NW, b, &bars[c]);
         }
     }
     __syncwarp();
 
-    const int x = st.xb + 4 * lane;
+    const int x = xb + 4 * lane;
     st.lane_out = lane >= HX / 4 && lane < 32 - HX / 4 && x < a.W;
     st.out_row0 = (src ? a.u0 : a.u1) + (int64_t)b * a.sstride + (int64_t)y0 * a.P + x;
     st.dmax = 0.0f;
@@ -165,7 +150,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
 #pragma unroll
     for (int s = 0; s < NW; ++s) win[s] = make_float4(0.f, 0.f, 0.f, 0.f);
 
-    for (int ib = 0; ib < st.nrows; ib += NW) block_steps<T, QOFF, RESID, 0>(win, ib, st);
+    for (int blk = 0; blk < nblk; ++blk) {
+        const int sg = blk % kStages;
+        mbar_wait(&bars[sg], (blk / kStages) & 1);
+        st.rows = ring + sg * STAGE_F;
+        block_steps<T, QOFF, RESID, 0>(win, blk * NW, st);
+        if (blk + kStages < nblk) {
+            __syncwarp();  // every lane has consumed stage sg (its values are in registers)
+            if (lane == 0) {
+                mbar_expect_tx(&bars[sg], STAGE_F * 4);
+                tma_load_3d(ring + sg * STAGE_F, tmap, xb, ystart + (blk + kStages) * NW, b, &bars[sg]);
+            }
+        }
+    }
 
     if (RESID) {
         const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(st.dmax));
@@ -241,7 +238,12 @@ static cudaError_t launch_T(const CUtensorMap& m0, const CUtensorMap& m1, const 
     const int nseg = a.seg_end - a.seg_begin;
     const int tasks = a.n_strips * nseg;
     dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta, B);
-    const size_t smem = kWarpsPerCta * kRingBytesPerWarp + kWarpsPerCta * kStages * sizeof(uint64_t);
+    const size_t smem = (size_t)kWarpsPerCta * kStages * (2 * T + 2) * kStripW * 4 + kWarpsPerCta * kStages * sizeof(uint64_t);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_rb_tblock<T, QOFF, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
     k_rb_tblock<T, QOFF, RESID><<<grid, kWarpsPerCta * 32, smem, st>>>(m0, m1, a);
     return cudaGetLastError();
 }

@@ -17,13 +17,12 @@ namespace twg {
 // ---------------------------------------------------------------- relaxation tiling
 // One warp owns a vertical strip of kStripW = 128 cells (4 per lane, one float4)
 // and `hseg` output rows.  Rows stream through a per-warp TMA ring of kStages
-// stages of kRingRows rows; the 2T half-sweeps of T red-black sweeps run as a
-// register wavefront.
+// stages of NW = 2T + 2 rows (one TMA box = one unrolled block of the row loop);
+// the 2T half-sweeps of T red-black sweeps run as a register wavefront
+// (DESIGN.md "k_rb_tblock").
 constexpr int kWarpsPerCta = 4;
 constexpr int kStripW = 128;
-constexpr int kRingRows = 4;
-constexpr int kStages = 4;
-constexpr int kRingBytesPerWarp = kStages * kRingRows * kStripW * 4;
+constexpr int kStages = 2;
 constexpr int kMaxT = 8;
 
 __host__ __device__ constexpr int halo_cols(int T) { return 4 * ((2 * T + 3) / 4); }  // round_up(2T, 4)
@@ -116,6 +115,7 @@ __device__ __forceinline__ bool is_free(float v) { return __float_as_int(v) < 0;
 
 // ---------------------------------------------------------------- context
 struct twg_ctx {
+    static constexpr int kMaxT = twg::kMaxT;
     int device = 0;
     cudaStream_t stream = nullptr;
     int W = 0, H = 0, B = 0, row_off = 0;
@@ -125,7 +125,7 @@ struct twg_ctx {
     float* u[2] = {nullptr, nullptr};
     std::vector<int> cur;          // per scenario: which buffer holds the current field
     int* d_cur = nullptr;          // device copy used by the tile kernel
-    CUtensorMap tmap[2];
+    CUtensorMap tmap[2][kMaxT + 1];  // [buffer][T]: box = 128 x (2T + 2) rows
     uint8_t* mask = nullptr;       // device [B][H][W]
     std::vector<uint8_t> hmask;    // host copy (validation only)
     // relaxation control, [B] each
