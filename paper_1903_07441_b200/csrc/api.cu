@@ -68,6 +68,20 @@ bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P, int 
     return r == CUDA_SUCCESS;
 }
 
+// The index matrix as {16 B, P / 16, H * B} uint8 with box {16, min(P, 512) / 16, 176}: one box
+// lands in shared memory as 176 rows of min(P, 512) contiguous bytes (k_walk windows).
+bool make_idx_map(CUtensorMap* m, uint8_t* base, int H, int B, int64_t P) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {16, (cuuint64_t)(P / 16), (cuuint64_t)H * (cuuint64_t)B};
+    cuuint64_t strides[2] = {16, (cuuint64_t)P};
+    cuuint32_t box[3] = {16, (cuuint32_t)(std::min<int64_t>(P, 512) / 16), 176};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <class T>
 cudaError_t dev_alloc(T** p, size_t n) {
     return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T));
@@ -511,6 +525,7 @@ twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg)
     p.meta = c->d_meta;
     p.idx = c->d_idx;
     p.istride = c->sstride;
+    p.idx_map = c->idx_map;
     int nl = 0;
     TWG_CUDA(c, launch_path(p, &nl, c->stream));
     c->launches += nl;
@@ -577,6 +592,8 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
         if (!make_tmap(&c->tmap[0][t], c->u[0], c->W, c->H, c->B, c->P, 2 * t + 2) ||
             !make_tmap(&c->tmap[1][t], c->u[1], c->W, c->H, c->B, c->P, 2 * t + 2))
             return bail(TWG_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point unavailable or bad layout)");
+    if (!make_idx_map(&c->idx_map, c->d_idx, c->H, c->B, c->P))
+        return bail(TWG_E_CUDA, "cuTensorMapEncodeTiled failed for the index matrix");
     CK(cudaStreamSynchronize(c->stream));
 #undef CK
     *out = c;

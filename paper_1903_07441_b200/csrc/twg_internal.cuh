@@ -160,6 +160,7 @@ struct twg_ctx {
     float2* d_smooth = nullptr;        // [B][smooth_cap]
     twg::PathMeta* d_meta = nullptr;   // [B]
     uint8_t* d_idx = nullptr;          // index matrix [B][H][P] bytes
+    CUtensorMap idx_map;               // TMA view of d_idx for the walker's windows
     // pinned host staging
     void* h_stage = nullptr;
     size_t h_stage_bytes = 0;

@@ -58,6 +58,7 @@ struct PathArgs {
     PathMeta* meta;        // [B]
     uint8_t* idx;          // index matrix M_idx, [B][H][P] bytes (Eq. 3)
     int64_t istride;       // bytes per scenario (H * P)
+    CUtensorMap idx_map;   // M_idx viewed as {16, P / 16, H * B} bytes, box {16, min(P, 512) / 16, 176}
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
 
