@@ -71,11 +71,18 @@ enum {
 
 /* Grid of `batch` independent scenarios of width x height cells of
  * cell_size metres (0.1 m), cell (0,0)'s corner at (origin_x,
- * origin_y).  row_offset: global index of local row 0 (row-slab sharding,
- * DESIGN.md "Multi-GPU"); red/black colour = parity of (x + row_offset + y)
- * (C1).  Single-GPU contexts pass 0. */
+ * origin_y).
+ * Row slabs: row_offset = global index of local row
+ * 0, so the red/black colour is the parity of (x + row_offset + y) (C1);
+ * ghost_rows = G rows at the top and at the bottom of the local grid that are
+ * copies of the neighbouring slabs (owned rows are [G, height - G)).  With
+ * G > 0 the residual of twg_relax covers the owned rows only, the goal and the
+ * robot may lie outside the local grid (their cells are then simply absent),
+ * and twg_extract_path / twg_plan_step are not available.  Single-GPU
+ * contexts pass 0 and 0. */
 typedef struct {
     int32_t width, height, batch, row_offset;
+    int32_t ghost_rows, reserved;
     double cell_size, origin_x, origin_y;
 } twg_grid_desc;
 

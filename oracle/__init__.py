@@ -73,6 +73,8 @@ def lib():
         L.orc_init_u64.argtypes = [i64, P, P]
         L.orc_relax_f32.restype = i32
         L.orc_relax_f32.argtypes = [i32, i32, P, P, i32, i32, f32, P]
+        L.orc_relax_f32_ex.restype = i32
+        L.orc_relax_f32_ex.argtypes = [i32, i32, P, P, i32, i32, f32, i32, i32, i32, P]
         L.orc_relax_f64.restype = i32
         L.orc_relax_f64.argtypes = [i32, i32, P, P, i32, i32, d, P]
         L.orc_jacobi_f64.restype = i32
@@ -190,6 +192,18 @@ def relax_f32(cls, u, max_sweeps, check_every=1, tol=0.0):
     H, W = u.shape
     r = np.zeros(1, np.float32)
     s = lib().orc_relax_f32(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol), _p(r))
+    return int(s), float(r[0])
+
+
+def relax_f32_ex(cls, u, max_sweeps, check_every=1, tol=0.0, row_parity=0, res_rows=None):
+    """relax_f32 with colour parity (x + row_parity + y) and the residual over rows res_rows only."""
+    assert u.dtype == np.float32 and u.flags.c_contiguous
+    cls = np.ascontiguousarray(cls, np.uint8)
+    H, W = u.shape
+    r0, r1 = res_rows if res_rows is not None else (0, H)
+    r = np.zeros(1, np.float32)
+    s = lib().orc_relax_f32_ex(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol),
+                               int(row_parity) & 1, int(r0), int(r1), _p(r))
     return int(s), float(r[0])
 
 

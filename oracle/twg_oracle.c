@@ -275,8 +275,11 @@ void orc_init_u64(int64_t ncell, const uint8_t* cls, double* u)
  * cells of sweep s.  Stop after sweep s when (s % check_every == 0 and
  * res_s < tol) or s == max_sweeps.  Returns sweeps done; *res_out = res_s of
  * the last sweep (0 if none). */
-int32_t orc_relax_f32(int32_t W, int32_t H, const uint8_t* cls, float* u,
-                      int32_t max_sweeps, int32_t check_every, float tol, float* res_out)
+/* General form used for row slabs: colour = parity of (x + row_parity + y); the residual is the
+ * max over the free cells of rows [res_r0, res_r1) only (the owned rows of a slab). */
+int32_t orc_relax_f32_ex(int32_t W, int32_t H, const uint8_t* cls, float* u, int32_t max_sweeps,
+                         int32_t check_every, float tol, int32_t row_parity, int32_t res_r0, int32_t res_r1,
+                         float* res_out)
 {
     float res = 0.0f;
     int32_t s = 0;
@@ -286,7 +289,7 @@ int32_t orc_relax_f32(int32_t W, int32_t H, const uint8_t* cls, float* u,
         for (int color = 0; color < 2; ++color)
             for (int32_t y = 0; y < H; ++y)
                 for (int32_t x = 0; x < W; ++x) {
-                    if (((x + y) & 1) != color) continue;
+                    if (((x + y + row_parity) & 1) != color) continue;
                     size_t q = (size_t)y * W + x;
                     if (cls[q] != ORC_FREE) continue;
                     float uE = x + 1 < W ? u[q + 1] : 0.0f;
@@ -295,7 +298,7 @@ int32_t orc_relax_f32(int32_t W, int32_t H, const uint8_t* cls, float* u,
                     float uS = y + 1 < H ? u[q + W] : 0.0f;
                     float nv = 0.25f * ((uE + uW) + (uN + uS));
                     float d = fabsf(nv - u[q]);
-                    if (d > res) res = d;
+                    if (d > res && y >= res_r0 && y < res_r1) res = d;
                     u[q] = nv;
                 }
         if ((s % check_every == 0 && res < tol) || s == max_sweeps) break;
@@ -303,6 +306,12 @@ int32_t orc_relax_f32(int32_t W, int32_t H, const uint8_t* cls, float* u,
     if (max_sweeps <= 0) { s = 0; res = 0.0f; }
     if (res_out) *res_out = res;
     return s;
+}
+
+int32_t orc_relax_f32(int32_t W, int32_t H, const uint8_t* cls, float* u,
+                      int32_t max_sweeps, int32_t check_every, float tol, float* res_out)
+{
+    return orc_relax_f32_ex(W, H, cls, u, max_sweeps, check_every, tol, 0, 0, H, res_out);
 }
 
 int32_t orc_relax_f64(int32_t W, int32_t H, const uint8_t* cls, double* u,

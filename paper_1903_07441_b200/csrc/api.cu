@@ -204,16 +204,18 @@ struct EncodeReq {
 
 // Host validation -> robot cell.
 twg_status validate(twg_ctx* c, const EncodeReq& r, int* rcx, int* rcy) {
-    if (r.gx < 0 || r.gy < 0 || r.gx >= c->W || r.gy >= c->H)
+    const bool slab = c->ghost > 0;  // goal and robot may belong to another slab
+    const bool g_in = r.gx >= 0 && r.gy >= 0 && r.gx < c->W && r.gy < c->H;
+    if (!g_in && !(slab && r.gx >= 0 && r.gx < c->W))
         return fail(c, TWG_E_OUT_OF_BOUNDS, "goal cell outside the grid");
     const uint8_t* m = c->hmask.data() + (size_t)r.b * c->H * c->W;
-    if (m[(size_t)r.gy * c->W + r.gx]) return fail(c, TWG_E_OVERLAPPING_CLASSES, "goal cell on a static wall");
+    if (g_in && m[(size_t)r.gy * c->W + r.gx]) return fail(c, TWG_E_OVERLAPPING_CLASSES, "goal cell on a static wall");
     const double fx = std::floor((r.robot.x - c->ox) / c->cs), fy = std::floor((r.robot.y - c->oy) / c->cs);
-    if (!(fx >= 0.0 && fy >= 0.0 && fx < (double)c->W && fy < (double)c->H))
-        return fail(c, TWG_E_OUT_OF_BOUNDS, "robot cell outside the grid");
-    *rcx = (int)fx;
-    *rcy = (int)fy;
-    if (m[(size_t)*rcy * c->W + *rcx]) return fail(c, TWG_E_INVALID_START, "robot cell on a static wall");
+    const bool r_in = fx >= 0.0 && fy >= 0.0 && fx < (double)c->W && fy < (double)c->H;
+    if (!r_in && !slab) return fail(c, TWG_E_OUT_OF_BOUNDS, "robot cell outside the grid");
+    *rcx = r_in ? (int)fx : -1;
+    *rcy = r_in ? (int)fy : -1;
+    if (r_in && m[(size_t)*rcy * c->W + *rcx]) return fail(c, TWG_E_INVALID_START, "robot cell on a static wall");
     if (r.n < 0) return fail(c, TWG_E_INVALID_ARG, "negative track count");
     return TWG_OK;
 }
@@ -407,6 +409,8 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
         a.H = c->H;
         a.done = c->d_done;
         a.res = c->d_res_bits;
+        a.res_r0 = c->ghost;
+        a.res_r1 = c->H - c->ghost;
         const int qoff = c->row_off & 1;
         int done_sw = 0, nchunk = 0;
         while (done_sw < maxs) {
@@ -540,6 +544,8 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     *out = nullptr;
     if (d->width <= 0 || d->height <= 0 || d->batch <= 0 || !(d->cell_size > 0.0))
         return fail(nullptr, TWG_E_INVALID_ARG, "width, height, batch > 0 and cell_size > 0 required");
+    if (d->ghost_rows < 0 || 2 * d->ghost_rows >= d->height)
+        return fail(nullptr, TWG_E_INVALID_ARG, "0 <= ghost_rows < height / 2 required");
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return fail(nullptr, TWG_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
     twg_ctx* c = new twg_ctx();
@@ -549,6 +555,7 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     c->H = d->height;
     c->B = d->batch;
     c->row_off = d->row_offset;
+    c->ghost = d->ghost_rows;
     c->cs = d->cell_size;
     c->ox = d->origin_x;
     c->oy = d->origin_y;
@@ -665,6 +672,7 @@ TWG_API twg_status twg_extract_path(twg_ctx* c, int32_t b, const twg_band_cfg* c
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad scenario index");
+    if (c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "path extraction is not available on a row slab");
     st = path(c, {b}, cfg);
     if (st != TWG_OK) return st;
     PathMeta* hm = nullptr;
@@ -698,6 +706,7 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
     if (st != TWG_OK) return st;
     if (!robot || !goal_xy || !n_tracks || !rcfg || !bcfg || !out || b < -1 || b >= c->B)
         return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    if (c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "twg_plan_step is not available on a row slab");
     std::vector<EncodeReq> reqs;
     std::vector<int> bs;
     int64_t off = 0;

@@ -54,7 +54,7 @@ __device__ __forceinline__ void half_sweep(float4& c, const float4& up, const fl
 // One wavefront step: row i of the strip (global row y = ystart + i) has landed in
 // win[S]; run half-sweeps k = 1..2T on rows y - k; store row y - 2T.
 template <int T, int QOFF, bool RESID, int S>
-__device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, int hs, bool lane_out,
+__device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, int hs, int rlo, int rhi, bool lane_out,
                                           float* __restrict__ out_row0, int64_t P, float& dmax) {
     constexpr int NW = 2 * T + 2;
     // all half-sweeps of this step update cells of one parity: q = (y + row_offset + 1) & 1
@@ -68,7 +68,7 @@ __device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, int h
             const int r = i - k - 2 * T;  // row index relative to the first output row
             float d = 0.0f;
             half_sweep<Qp, true>(win[c], win[up], win[dn], d);
-            if (lane_out && r >= 0 && r < hs) dmax = fmaxf(dmax, d);
+            if (lane_out && r >= rlo && r < rhi) dmax = fmaxf(dmax, d);
         } else {
             float d = 0.0f;
             half_sweep<Qp, false>(win[c], win[up], win[dn], d);
@@ -87,6 +87,7 @@ struct Strip {
     float* out_row0;
     int64_t P;
     int hs, lane;
+    int rlo, rhi;       // rows (relative to the first output row) that count in the residual
     bool lane_out;
     float dmax;
 };
@@ -97,7 +98,7 @@ struct Strip {
 template <int T, int QOFF, bool RESID, int S>
 __device__ __forceinline__ void block_steps(float4 (&win)[2 * T + 2], int ib, Strip& st) {
     win[S] = reinterpret_cast<const float4*>(st.rows + S * kStripW)[st.lane];
-    wave_step<T, QOFF, RESID, S>(win, ib + S, st.hs, st.lane_out, st.out_row0, st.P, st.dmax);
+    wave_step<T, QOFF, RESID, S>(win, ib + S, st.hs, st.rlo, st.rhi, st.lane_out, st.out_row0, st.P, st.dmax);
     if constexpr (S + 1 < 2 * T + 2) block_steps<T, QOFF, RESID, S + 1>(win, ib, st);
 }
 
@@ -122,6 +123,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     const int y0 = seg * a.hseg;       // first output row, even
     Strip st;
     st.hs = min(a.hseg, a.H - y0);
+    st.rlo = max(0, a.res_r0 - y0);
+    st.rhi = min(st.hs, a.res_r1 - y0);
     const int ystart = y0 - 2 * T;
     const int nblk = (st.hs + 4 * T + NW - 1) / NW;  // rows ystart .. ystart + nblk*NW - 1
     st.lane = lane;

@@ -51,7 +51,7 @@ __global__ void k_goal_reset(EncodeArgs e) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= e.nscen) return;
     const ScenParams& sp = e.params[k];
-    if (!sp.warm || sp.old_gx < 0) return;
+    if (!sp.warm || sp.old_gx < 0 || sp.old_gy < 0 || sp.old_gy >= e.H) return;
     if (sp.old_gx == sp.gx && sp.old_gy == sp.gy) return;
     const int b = sp.b;
     if (e.mask[((int64_t)b * e.H + sp.old_gy) * e.W + sp.old_gx]) return;
@@ -183,6 +183,7 @@ __global__ void k_set_goal(EncodeArgs e) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= e.nscen) return;
     const ScenParams& sp = e.params[k];
+    if (sp.gy < 0 || sp.gy >= e.H) return;  // the goal lies in another row slab
     (sp.cur ? e.u1 : e.u0)[(int64_t)sp.b * e.sstride + (int64_t)sp.gy * e.P + sp.gx] = 1.0f;
 }
 

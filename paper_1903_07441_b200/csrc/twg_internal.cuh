@@ -38,6 +38,7 @@ struct RelaxArgs {
     int W, H;
     int n_strips, hseg;
     int seg_begin, seg_end;  // launched segment range
+    int res_r0, res_r1;  // rows whose cells count in the residual (owned rows of a slab)
     const int* done;     // per-scenario done flags
     unsigned* res;       // per-scenario residual (float bits, atomicMax), used when RESID
 };
@@ -118,7 +119,7 @@ struct twg_ctx {
     static constexpr int kMaxT = twg::kMaxT;
     int device = 0;
     cudaStream_t stream = nullptr;
-    int W = 0, H = 0, B = 0, row_off = 0;
+    int W = 0, H = 0, B = 0, row_off = 0, ghost = 0;
     double cs = 0.1, ox = 0.0, oy = 0.0;
     int64_t P = 0;        // pitch in floats
     int64_t sstride = 0;  // floats per scenario field

@@ -1,0 +1,202 @@
+"""Row-slab decomposition of the relaxation across ranks (BASELINE.json configs[3]).
+
+Each rank owns a contiguous block of global rows [r0, r1) and keeps G = 2k ghost rows above and
+below it.  It relaxes its local grid (owned + ghosts) for k sweeps with ``twg_relax``; rows within
+2k of the local edge are then stale, which is exactly the ghost region, so the owned rows are
+bit-identical to a single-grid relaxation (the outermost ghost row is read-only and the inner
+2k - 1 are recomputed redundantly; SURVEY.md §0 finding 6).  Then the 2k owned boundary rows are
+sent to each neighbour and its ghost rows received (NCCL point-to-point through
+``torch.distributed`` on GPUs, gloo on the CPU).  At check sweeps the owned-row residuals are
+max-all-reduced, so every rank applies the same stop rule (C6).  Colours stay global because
+each slab is created with ``row_offset = r0 - G`` (C1).
+
+The compute backend is pluggable (``relax(n) -> residual``, ``field_view() -> [rows, pitch]``):
+:class:`TwgSlabBackend` wraps a libtwg context; the CPU tests drive the same schedule with the
+oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def slab_rows(H: int, world: int, rank: int):
+    """Owned global rows [r0, r1) of `rank` (near-equal contiguous split)."""
+    base, extra = divmod(H, world)
+    r0 = rank * base + min(rank, extra)
+    return r0, r0 + base + (1 if rank < extra else 0)
+
+
+@dataclass
+class SlabLayout:
+    W: int
+    H_global: int
+    world: int
+    rank: int
+    k: int  # sweeps between ghost exchanges
+
+    def __post_init__(self):
+        self.G = 2 * self.k
+        self.r0, self.r1 = slab_rows(self.H_global, self.world, self.rank)
+        if self.r1 - self.r0 < self.G:
+            raise ValueError(f"slab of {self.r1 - self.r0} rows is thinner than 2k = {self.G}")
+        self.local_h = self.r1 - self.r0 + 2 * self.G
+        self.row_offset = self.r0 - self.G  # global index of local row 0
+
+    # local row ranges
+    def ghost_top(self):
+        return 0, self.G
+
+    def owned_top(self):
+        return self.G, 2 * self.G
+
+    def owned_bottom(self):
+        return self.local_h - 2 * self.G, self.local_h - self.G
+
+    def ghost_bottom(self):
+        return self.local_h - self.G, self.local_h
+
+    def global_rows(self):
+        """Global rows covered by the local grid (ghost rows outside the grid are padding)."""
+        return self.row_offset, self.row_offset + self.local_h
+
+    def local_slice(self, global_array, fill):
+        """Rows row_offset .. row_offset + local_h of a global [H, W] array; rows outside -> fill."""
+        out = np.full((self.local_h,) + global_array.shape[1:], fill, dtype=global_array.dtype)
+        g0, g1 = self.global_rows()
+        a, b = max(g0, 0), min(g1, self.H_global)
+        out[a - g0:b - g0] = global_array[a:b]
+        return out
+
+
+def interval_schedule(max_sweeps: int, k: int, check_every: int = 0, tol: float = 0.0):
+    """Yield (n, is_check): n sweeps between exchanges, never crossing a check sweep."""
+    ce = check_every if (tol > 0 and check_every > 0) else max(max_sweeps, 1)
+    s = 0
+    while s < max_sweeps:
+        nxt = (s // ce + 1) * ce
+        n = min(k, nxt - s, max_sweeps - s)
+        s += n
+        yield n, (s % ce == 0) or s == max_sweeps, s
+
+
+class DistExchanger:
+    """Ghost exchange and residual reduction over torch.distributed (NCCL or gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def exchange(self, lay: SlabLayout, field):
+        d = self.dist
+        ops = []
+        if lay.rank > 0:
+            a, b = lay.owned_top()
+            ops.append(d.P2POp(d.isend, field[a:b].contiguous(), lay.rank - 1, self.group))
+            ga, gb = lay.ghost_top()
+            top = field[ga:gb]
+            rt = top if top.is_contiguous() else top.contiguous()
+            ops.append(d.P2POp(d.irecv, rt, lay.rank - 1, self.group))
+        if lay.rank < lay.world - 1:
+            a, b = lay.owned_bottom()
+            ops.append(d.P2POp(d.isend, field[a:b].contiguous(), lay.rank + 1, self.group))
+            ga, gb = lay.ghost_bottom()
+            bot = field[ga:gb]
+            rb = bot if bot.is_contiguous() else bot.contiguous()
+            ops.append(d.P2POp(d.irecv, rb, lay.rank + 1, self.group))
+        if ops:
+            for r in d.batch_isend_irecv(ops):
+                r.wait()
+
+    def allreduce_max(self, value: float, device=None) -> float:
+        import torch
+        t = torch.tensor([value], dtype=torch.float32, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+class SlabRelaxer:
+    """Runs the k-sweep interval schedule of one rank."""
+
+    def __init__(self, backend, layout: SlabLayout, exchanger, device=None):
+        self.backend, self.lay, self.ex, self.device = backend, layout, exchanger, device
+
+    def relax(self, max_sweeps: int, check_every: int = 0, tol: float = 0.0):
+        res, s = 0.0, 0
+        for n, is_check, s in interval_schedule(max_sweeps, self.lay.k, check_every, tol):
+            r = self.backend.relax(n)
+            if is_check:
+                res = self.ex.allreduce_max(r, self.device)
+            if s < max_sweeps:
+                self.ex.exchange(self.lay, self.backend.field_view())
+            if is_check and tol > 0 and check_every > 0 and s % check_every == 0 and res < tol:
+                break
+        return s, res
+
+
+class _CudaView:
+    """Zero-copy torch view of a device buffer (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr, shape, typestr="<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class TwgSlabBackend:
+    """libtwg context holding one slab: local grid = owned rows + 2G ghost rows."""
+
+    def __init__(self, planner, device=0):
+        self.pl = planner
+        self.device = device
+
+    def relax(self, n: int) -> float:
+        from .twg import relax_cfg
+        _, res = self.pl.relax(relax_cfg(max_sweeps=n))
+        return float(res[0])
+
+    def field_view(self):
+        import torch
+        ptr, pitch = self.pl.field_ptr(0)
+        return torch.as_tensor(_CudaView(ptr, (self.pl.H, pitch)), device=f"cuda:{self.device}")
+
+
+def make_twg_slab(layout: SlabLayout, static_global, robot, goal, tracks, warp, cell_size=0.1,
+                  origin=(0.0, 0.0), device=0, stream=None):
+    """Create and encode (cold) the libtwg context of one slab from the global scene.
+
+    Local row 0 is global row ``layout.row_offset``; ghost rows outside the global grid are walls
+    (outside = obstacle, C4).  The goal is passed in local coordinates (it may lie outside)."""
+    from .twg import Planner
+    pl = Planner(layout.W, layout.local_h, 1, cell_size, (origin[0], origin[1] + layout.row_offset * cell_size),
+                 device=device, stream=stream, row_offset=layout.row_offset, ghost_rows=layout.G)
+    pl.set_static(np.ascontiguousarray(layout.local_slice(np.asarray(static_global, np.uint8), 1)))
+    pl.set_obstacles(0, robot, (goal[0], goal[1] - layout.row_offset), tracks, warp, warm=0)
+    return pl
+
+
+def relax_local_slabs(backends, layouts, max_sweeps: int, check_every: int = 0, tol: float = 0.0):
+    """All slabs in one process (e.g. several contexts on one GPU): the same interval schedule,
+    ghost rows copied between the slabs' buffers, residual = max over slabs."""
+    k = layouts[0].k
+    res, s = 0.0, 0
+    for n, is_check, s in interval_schedule(max_sweeps, k, check_every, tol):
+        rs = [b.relax(n) for b in backends]
+        if is_check:
+            res = max(rs)
+        if s < max_sweeps:
+            views = [b.field_view() for b in backends]
+            for r in range(len(backends) - 1):
+                up, dn, lu, ld = views[r], views[r + 1], layouts[r], layouts[r + 1]
+                a, b = lu.owned_bottom()
+                ga, gb = ld.ghost_top()
+                top_src = up[a:b].clone()
+                a2, b2 = ld.owned_top()
+                ga2, gb2 = lu.ghost_bottom()
+                bot_src = dn[a2:b2].clone()
+                dn[ga:gb].copy_(top_src)
+                up[ga2:gb2].copy_(bot_src)
+        if is_check and tol > 0 and check_every > 0 and s % check_every == 0 and res < tol:
+            break
+    return s, res

@@ -23,6 +23,7 @@ E_NO_PATH, E_CUDA, E_NCCL, E_NO_MEMORY = -5, -6, -7, -8
 
 class GridDesc(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("batch", C.c_int32), ("row_offset", C.c_int32),
+                ("ghost_rows", C.c_int32), ("reserved", C.c_int32),
                 ("cell_size", C.c_double), ("origin_x", C.c_double), ("origin_y", C.c_double)]
 
 
@@ -152,9 +153,11 @@ class Planner:
     """Owns one twg_ctx.  Method names mirror the C ABI (twg_<name>)."""
 
     def __init__(self, width, height, batch=1, cell_size=0.1, origin=(0.0, 0.0), device=0, stream=None,
-                 row_offset=0):
+                 row_offset=0, ghost_rows=0):
         self.W, self.H, self.B = int(width), int(height), int(batch)
-        d = GridDesc(self.W, self.H, self.B, int(row_offset), float(cell_size), float(origin[0]), float(origin[1]))
+        self.row_offset, self.ghost_rows = int(row_offset), int(ghost_rows)
+        d = GridDesc(self.W, self.H, self.B, self.row_offset, self.ghost_rows, 0, float(cell_size),
+                     float(origin[0]), float(origin[1]))
         h = C.c_void_p()
         st = lib().twg_create(C.byref(d), int(device), stream, C.byref(h))
         if st != OK:
