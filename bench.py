@@ -221,6 +221,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         l0 = pl.kernel_launches()
         walk = []
+        torch.cuda.nvtx.range_push("timed_region_host" if host else "timed_region")
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
             ev[k][0].record(stream)
@@ -228,6 +229,7 @@ def run_ours(args):
             ev[k][1].record(stream)
             walk.append(r[0].walk_status)
         torch.cuda.synchronize(dev)
+        torch.cuda.nvtx.range_pop()
         launches = pl.kernel_launches() - l0
         ms = sum(a.elapsed_time(b) for a, b in ev)
         if ws > 1:

@@ -119,8 +119,9 @@ typedef struct {
  *   max|du| of sweep s is evaluated when s % check_every == 0 or s ==
  *   max_sweeps (C5); stop early when it is < tol (tol <= 0: fixed budget,
  *   C6); warm_start [1]: used by twg_plan_step's encode (C7);
- *   temporal_depth [0 = auto]: sweeps fused per tile load (T);
- *   rows_per_warp [0 = auto]: rows of the strip one warp owns;
+ *   temporal_depth [0 = auto = 6]: sweeps fused per tile load (T, 1..8);
+ *   rows_per_warp [0 = auto, load model of DESIGN.md]: rows of the strip one
+ *   warp owns;
  *   sync_every [64]: convergence flags are read back every sync_every
  *   checks when tol > 0. */
 typedef struct {

@@ -349,26 +349,35 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     return TWG_OK;
 }
 
-// Output rows per warp.  hseg + 4T is made a multiple of NW = 2T + 2 (the kernel streams whole
-// NW-row blocks, so any other value pays for padded rows); hseg is even (colour parity of the
-// first row is a compile-time constant).
-int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows) {
+// Output rows per warp (hseg).  hseg + 4T is a multiple of NW = 2T + 2 (the kernel streams whole
+// NW-row blocks, so any other value pays for padded rows) and even (the colour parity of the first
+// row is a compile-time constant).  Among those, pick the one minimising the load model measured on
+// B200: a launch takes ~ (CTAs on the busiest SM) x (hseg + 4T) /
+// min(CTAs per SM, 2) -- throughput saturates at two 4-warp CTAs per SM.
+int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows, int n_sm) {
     const int NW = 2 * T + 2;
-    int h;
     if (cfg_rows > 0) {
-        h = cfg_rows;
-    } else {
-        const int target = 148 * 16;  // warps per launch (4 CTAs x 4 warps per SM)
-        int segs = (target + n_strips * nscen - 1) / (n_strips * nscen);
-        segs = std::max(segs, 1);
-        h = (H + segs - 1) / segs;
-        h = std::max(h, 8 * T);
-        const int k = std::max(1, (h + 4 * T + NW / 2) / NW);
-        h = std::max(k * NW - 4 * T, 2);
+        int h = std::min(cfg_rows, H);
+        h = (h + 1) & ~1;
+        return std::max(h, 2);
     }
-    h = std::min(h, H);
-    h = (h + 1) & ~1;
-    return std::max(h, 2);
+    int best_h = 2;
+    double best = 1e300;
+    for (int k = 1; k <= 256; ++k) {
+        const int h = k * NW - 4 * T;
+        if (h < 2) continue;
+        const int hh = std::min(h, (H + 1) & ~1);
+        const long long segs = (H + hh - 1) / hh;
+        const long long ctas = (segs * n_strips * nscen + kWarpsPerCta - 1) / kWarpsPerCta;
+        const long long per_sm = (ctas + n_sm - 1) / n_sm;
+        const double cost = (double)per_sm * (hh + 4 * T) / (double)std::min<long long>(per_sm, 2);
+        if (cost < best * 0.999) {
+            best = cost;
+            best_h = hh;
+        }
+        if (h >= H) break;
+    }
+    return std::max(best_h, 2);
 }
 
 // Rows a4-a6 for the scenarios whose participation flag is set.
@@ -378,7 +387,7 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
     const int maxs = cfg->max_sweeps;
     if (maxs < 0 || cfg->check_every < 0) return fail(c, TWG_E_INVALID_ARG, "negative sweep counts");
     const int B = c->B;
-    int T = cfg->temporal_depth > 0 ? std::min(cfg->temporal_depth, kMaxT) : 4;
+    int T = cfg->temporal_depth > 0 ? std::min(cfg->temporal_depth, kMaxT) : 6;
     const float tol = cfg->tol;
     int check = (tol > 0.0f && cfg->check_every > 0) ? cfg->check_every : std::max(maxs, 1);
     const int sync_every = cfg->sync_every > 0 ? cfg->sync_every : 64;
@@ -422,7 +431,7 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
             for (size_t q = 0; q < plan.size(); ++q) {
                 const int t = plan[q];
                 a.n_strips = (c->W + out_cols(t) - 1) / out_cols(t);
-                a.hseg = auto_hseg(t, c->H, a.n_strips, std::max(nscen, 1), cfg->rows_per_warp);
+                a.hseg = auto_hseg(t, c->H, a.n_strips, std::max(nscen, 1), cfg->rows_per_warp, c->n_sm);
                 a.seg_begin = 0;
                 a.seg_end = (c->H + a.hseg - 1) / a.hseg;
                 a.lp = lp & 1;
@@ -551,6 +560,8 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     twg_ctx* c = new twg_ctx();
     c->device = device;
     c->stream = static_cast<cudaStream_t>(stream);
+    if (cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || c->n_sm <= 0)
+        c->n_sm = 148;
     c->W = d->width;
     c->H = d->height;
     c->B = d->batch;

@@ -52,10 +52,11 @@ __device__ __forceinline__ void half_sweep(float4& c, const float4& up, const fl
 }
 
 // One wavefront step: row i of the strip (global row y = ystart + i) has landed in
-// win[S]; run half-sweeps k = 1..2T on rows y - k; store row y - 2T.
+// win[S]; run half-sweeps k = 1..2T on rows y - k; store row y - 2T through the running
+// output pointer `op` (row i - 4T of the segment; advanced by one pitch per step).
 template <int T, int QOFF, bool RESID, int S>
-__device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, int hs, int rlo, int rhi, bool lane_out,
-                                          float* __restrict__ out_row0, int64_t P, float& dmax) {
+__device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, unsigned hs, int rlo, unsigned rn,
+                                          bool lane_out, float*& op, int64_t P, float& dmax) {
     constexpr int NW = 2 * T + 2;
     // all half-sweeps of this step update cells of one parity: q = (y + row_offset + 1) & 1
     constexpr int Qp = (S + 1 + QOFF) & 1;
@@ -68,26 +69,26 @@ __device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, int h
             const int r = i - k - 2 * T;  // row index relative to the first output row
             float d = 0.0f;
             half_sweep<Qp, true>(win[c], win[up], win[dn], d);
-            if (lane_out && r >= rlo && r < rhi) dmax = fmaxf(dmax, d);
+            if (lane_out && (unsigned)(r - rlo) < rn) dmax = fmaxf(dmax, d);
         } else {
             float d = 0.0f;
             half_sweep<Qp, false>(win[c], win[up], win[dn], d);
         }
     }
-    const int ro = i - 4 * T;  // output row (relative) finalised by this step
-    if (lane_out && ro >= 0 && ro < hs) {
-        constexpr int so = (S - 2 * T + 2 * NW) % NW;
-        *reinterpret_cast<float4*>(out_row0 + (int64_t)ro * P) = win[so];
-    }
+    constexpr int so = (S - 2 * T + 2 * NW) % NW;
+    if (lane_out && (unsigned)(i - 4 * T) < hs) *reinterpret_cast<float4*>(op) = win[so];
+    op += P;
 }
 
 // Per-warp streaming state of k_rb_tblock.
 struct Strip {
     const float* rows;  // current ring stage: NW rows x 128 floats
-    float* out_row0;
+    float* op;          // output pointer of the row finalised by the next step
     int64_t P;
-    int hs, lane;
-    int rlo, rhi;       // rows (relative to the first output row) that count in the residual
+    unsigned hs;        // output rows of this segment
+    int lane;
+    int rlo;            // first row (relative to the first output row) counted in the residual
+    unsigned rn;        // number of rows counted in the residual
     bool lane_out;
     float dmax;
 };
@@ -98,7 +99,7 @@ struct Strip {
 template <int T, int QOFF, bool RESID, int S>
 __device__ __forceinline__ void block_steps(float4 (&win)[2 * T + 2], int ib, Strip& st) {
     win[S] = reinterpret_cast<const float4*>(st.rows + S * kStripW)[st.lane];
-    wave_step<T, QOFF, RESID, S>(win, ib + S, st.hs, st.rlo, st.rhi, st.lane_out, st.out_row0, st.P, st.dmax);
+    wave_step<T, QOFF, RESID, S>(win, ib + S, st.hs, st.rlo, st.rn, st.lane_out, st.op, st.P, st.dmax);
     if constexpr (S + 1 < 2 * T + 2) block_steps<T, QOFF, RESID, S + 1>(win, ib, st);
 }
 
@@ -122,11 +123,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     const int xb = strip * WOUT - HX;  // first (halo) column of the strip, even
     const int y0 = seg * a.hseg;       // first output row, even
     Strip st;
-    st.hs = min(a.hseg, a.H - y0);
+    const int hs = min(a.hseg, a.H - y0);
+    st.hs = (unsigned)hs;
     st.rlo = max(0, a.res_r0 - y0);
-    st.rhi = min(st.hs, a.res_r1 - y0);
+    st.rn = (unsigned)max(0, min(hs, a.res_r1 - y0) - st.rlo);
     const int ystart = y0 - 2 * T;
-    const int nblk = (st.hs + 4 * T + NW - 1) / NW;  // rows ystart .. ystart + nblk*NW - 1
+    const int nblk = (hs + 4 * T + NW - 1) / NW;  // rows ystart .. ystart + nblk*NW - 1
     st.lane = lane;
     st.P = a.P;
 
@@ -147,7 +149,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
 
     const int x = xb + 4 * lane;
     st.lane_out = lane >= HX / 4 && lane < 32 - HX / 4 && x < a.W;
-    st.out_row0 = (src ? a.u0 : a.u1) + (int64_t)b * a.sstride + (int64_t)y0 * a.P + x;
+    // row i - 4T of the segment is finalised at step i: start 4T rows above the first output row
+    st.op = (src ? a.u0 : a.u1) + (int64_t)b * a.sstride + (int64_t)(y0 - 4 * T) * a.P + x;
     st.dmax = 0.0f;
     float4 win[NW];
 #pragma unroll

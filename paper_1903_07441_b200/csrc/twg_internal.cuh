@@ -118,6 +118,7 @@ __device__ __forceinline__ bool is_free(float v) { return __float_as_int(v) < 0;
 struct twg_ctx {
     static constexpr int kMaxT = twg::kMaxT;
     int device = 0;
+    int n_sm = 148;
     cudaStream_t stream = nullptr;
     int W = 0, H = 0, B = 0, row_off = 0, ghost = 0;
     double cs = 0.1, ox = 0.0, oy = 0.0;
