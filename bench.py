@@ -56,6 +56,11 @@ def _args():
     ap.add_argument("--obstacles", type=int, default=200)
     ap.add_argument("--prep-sweeps", type=int, default=4_000_000,
                     help="untimed cold solve before the timed warm ticks (stops at the exact fp32 fixed point)")
+    ap.add_argument("--config", default="c3", choices=["c3", "c4", "c5"],
+                    help="c3: 4096^2 plan step (default, headline); c4: 16384^2 row slabs over the ranks; "
+                         "c5: 1024 x 512^2 scenarios split over the ranks")
+    ap.add_argument("--k", type=int, default=12, help="c4: sweeps between ghost exchanges")
+    ap.add_argument("--batch", type=int, default=1024, help="c5: total scenarios")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     return ap.parse_args()
@@ -304,10 +309,159 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------- C4: row slabs
+def run_c4(args):
+    """16384^2 relaxation, rows split over the ranks, 2k ghost rows exchanged every k sweeps
+    (NCCL point-to-point), residual max-all-reduced at the end.  Strong scaling."""
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1903_07441_b200 import warp_cfg, lib
+    from paper_1903_07441_b200.slab import SlabLayout, SlabRelaxer, TwgSlabBackend, DistExchanger, make_twg_slab
+    from scenes import scene_c4
+    lib()
+    sc = scene_c4(0)
+    lay = SlabLayout(sc.W, sc.H, ws, rank, args.k)
+    stream = torch.cuda.current_stream(dev)
+    pl = make_twg_slab(lay, sc.static, sc.robot, sc.goal, sc.tracks, warp_cfg(), device=local, stream=stream.cuda_stream)
+    be = TwgSlabBackend(pl, local)
+
+    class _Single:  # world size 1: nothing to exchange
+        def exchange(self, lay, field):
+            pass
+
+        def allreduce_max(self, v, device=None):
+            return v
+
+    relaxer = SlabRelaxer(be, lay, DistExchanger() if ws > 1 else _Single(), device=dev)
+    S = args.relax_sweeps
+    relaxer.relax(2 * args.k)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms_tot = 0.0
+    l0 = pl.kernel_launches()
+    with Clocks(local, enabled=not args.no_clocks) as clk:
+        for _ in range(args.steps):
+            e0.record(stream)
+            s, res = relaxer.relax(S)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms_tot += e0.elapsed_time(e1)
+    launches = pl.kernel_launches() - l0
+    if ws > 1:
+        t = torch.tensor([ms_tot], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_tot = float(t.item())
+    value = sc.W * sc.H * S * args.steps / (ms_tot * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({"metric": "harmonic relaxation GLUP/s at 16384^2 (row slabs)", "value": value, "unit": UNIT,
+                          "n_gpus": ws, "steps": args.steps, "warmup": 1, "ms_per_step": ms_tot / args.steps,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                          "data": "synthetic",
+                          "config": {"workload": f"c4_16384: {sc.W}x{sc.H} grid, {sc.n_tracks} obstacles, relax "
+                                                 f"{S} sweeps per step, ghost exchange every k={args.k} sweeps",
+                                     "k": args.k, "ghost_rows": lay.G, "rows_per_rank": lay.r1 - lay.r0},
+                          "gpu_launches": int(launches), "residual": res, "clocks": clk.summary()}), flush=True)
+    pl.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------- C5: batch
+def run_c5(args):
+    """1024 independent 512^2 scenarios, 1024/N per rank in one batched context (weak in the
+    scenarios per rank).  A step = twg_plan_step(b = -1) with S = 100 warm sweeps."""
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1903_07441_b200 import Planner, band_cfg, relax_cfg, warp_cfg, lib
+    from scenes import scene_random, advance_scene
+    lib()
+    per = args.batch // ws
+    scs = [scene_random(f"c5_s{s}", 512, 8, 20, s) for s in range(rank * per, (rank + 1) * per)]
+    stream = torch.cuda.current_stream(dev)
+    pl = Planner(512, 512, per, 0.1, (0.0, 0.0), device=local, stream=stream.cuda_stream)
+    for b, sc in enumerate(scs):
+        pl.set_static(sc.static, b)
+    wc, bc = warp_cfg(), band_cfg(args.band_iters, 4096, 8192)
+
+    ticks = {}
+
+    def inputs(tick):  # scene advance and packing are input generation: done before the timed region
+        if tick not in ticks:
+            ss = [advance_scene(sc, tick) for sc in scs]
+            ticks[tick] = ([s.robot for s in ss], [s.goal for s in ss],
+                           torch.from_numpy(np.ascontiguousarray(np.vstack([s.tracks for s in ss]))).pin_memory(),
+                           [s.n_tracks for s in ss])
+        return ticks[tick]
+
+    def step(tick, rc):
+        rob, goals, tr, nt = inputs(tick)
+        return pl.plan_step(-1, rob, goals, tr, nt, wc, rc, bc, want_paths=False)
+
+    for k in range(1 + args.warmup + args.steps):
+        inputs(k)
+
+    t_prep = time.perf_counter()
+    step(0, relax_cfg(max_sweeps=100000, check_every=2000, tol=1e-38, warm_start=0, sync_every=4))
+    prep_s = time.perf_counter() - t_prep
+    rc = relax_cfg(max_sweeps=args.sweeps, warm_start=1)
+    for k in range(args.warmup):
+        step(1 + k, rc)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    ms_tot, ok = 0.0, 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local, enabled=not args.no_clocks) as clk:
+        for k in range(args.steps):
+            torch.cuda.nvtx.range_push("timed_region")
+            e0.record(stream)
+            st, res, _, _ = step(1 + args.warmup + k, rc)
+            torch.cuda.nvtx.range_pop()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms_tot += e0.elapsed_time(e1)
+            ok += sum(1 for r in res if r.walk_status == 0)
+    if ws > 1:
+        t = torch.tensor([ms_tot], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_tot = float(t.item())
+    value = 512 * 512 * per * ws * args.sweeps * args.steps / (ms_tot * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({"metric": "harmonic relaxation GLUP/s, batch of 512^2 plan steps", "value": value,
+                          "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": ms_tot / args.steps, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                          "config": {"workload": f"c5: {args.batch} x 512x512 scenarios (20 obstacles each), "
+                                                 f"{per} per rank, warm plan step S={args.sweeps}, "
+                                                 f"I={args.band_iters} (host tracks include per-step H2D)"},
+                          "scenario_steps_per_s": per * ws * args.steps / (ms_tot * 1e-3),
+                          "walk_ok_fraction": ok / (args.steps * per), "prep_s": prep_s,
+                          "clocks": clk.summary()}), flush=True)
+    pl.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = _args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c4":
+        run_c4(args)
+    elif args.config == "c5":
+        run_c5(args)
     else:
         run_ours(args)
 

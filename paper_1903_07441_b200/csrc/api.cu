@@ -261,37 +261,45 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     if (st != TWG_OK) return st;
     st = ensure_params(c, ns);
     if (st != TWG_OK) return st;
-    // tracks -> [B][cap]
+    // tracks -> [B][cap]: one contiguous copy (device input: in place; host input: through the pinned
+    // staging ring and one H2D copy) and one scatter kernel for every scenario of the call
     if (total > 0) {
-        if (is_device_ptr(tracks)) {
-            std::vector<int> off(ns + 1), sb(ns);
-            for (int k = 0; k < ns; ++k) {
-                off[k] = (int)reqs[k].track_off;
-                sb[k] = reqs[k].b;
+        const twg_track* src = tracks;
+        if (!is_device_ptr(tracks)) {
+            if (c->track_tmp_cap < total) {
+                if (c->d_track_tmp) cudaFree(c->d_track_tmp);
+                c->d_track_tmp = nullptr;
+                TWG_CUDA(c, dev_alloc(&c->d_track_tmp, (size_t)total));
+                c->track_tmp_cap = total;
             }
-            off[ns] = (int)(reqs[ns - 1].track_off + reqs[ns - 1].n);
-            if (c->track_off_cap < 2 * ns + 1) {
-                if (c->d_track_off) cudaFree(c->d_track_off);
-                c->d_track_off = nullptr;
-                TWG_CUDA(c, dev_alloc(&c->d_track_off, 2 * ns + 1));
-                c->track_off_cap = 2 * ns + 1;
-            }
-            int* hs = nullptr;
-            TWG_CUDA(c, stage_alloc(c, (2 * ns + 1) * sizeof(int), reinterpret_cast<void**>(&hs)));
-            std::memcpy(hs, off.data(), (ns + 1) * sizeof(int));
-            std::memcpy(hs + ns + 1, sb.data(), ns * sizeof(int));
-            TWG_CUDA(c, cudaMemcpyAsync(c->d_track_off, hs, (2 * ns + 1) * sizeof(int), cudaMemcpyHostToDevice,
+            twg_track* ht = nullptr;
+            TWG_CUDA(c, stage_alloc(c, (size_t)total * sizeof(twg_track), reinterpret_cast<void**>(&ht)));
+            int64_t first = reqs[0].track_off;
+            std::memcpy(ht, tracks + first, (size_t)total * sizeof(twg_track));
+            TWG_CUDA(c, cudaMemcpyAsync(c->d_track_tmp, ht, (size_t)total * sizeof(twg_track), cudaMemcpyHostToDevice,
                                         c->stream));
-            TWG_CUDA(c, launch_scatter_tracks(tracks, c->d_track_off, ns, c->d_track_off + ns + 1, c->d_tracks,
-                                              c->track_cap, c->stream));
-            c->launches += 1;
-        } else {
-            for (int k = 0; k < ns; ++k)
-                if (reqs[k].n > 0)
-                    TWG_CUDA(c, cudaMemcpyAsync(c->d_tracks + (int64_t)reqs[k].b * c->track_cap,
-                                                tracks + reqs[k].track_off, reqs[k].n * sizeof(twg_track),
-                                                cudaMemcpyHostToDevice, c->stream));
+            src = c->d_track_tmp - first;  // offsets below are relative to the caller's array
         }
+        std::vector<int> off(ns + 1), sb(ns);
+        for (int k = 0; k < ns; ++k) {
+            off[k] = (int)reqs[k].track_off;
+            sb[k] = reqs[k].b;
+        }
+        off[ns] = (int)(reqs[ns - 1].track_off + reqs[ns - 1].n);
+        if (c->track_off_cap < 2 * ns + 1) {
+            if (c->d_track_off) cudaFree(c->d_track_off);
+            c->d_track_off = nullptr;
+            TWG_CUDA(c, dev_alloc(&c->d_track_off, 2 * ns + 1));
+            c->track_off_cap = 2 * ns + 1;
+        }
+        int* hs = nullptr;
+        TWG_CUDA(c, stage_alloc(c, (2 * ns + 1) * sizeof(int), reinterpret_cast<void**>(&hs)));
+        std::memcpy(hs, off.data(), (ns + 1) * sizeof(int));
+        std::memcpy(hs + ns + 1, sb.data(), ns * sizeof(int));
+        TWG_CUDA(c, cudaMemcpyAsync(c->d_track_off, hs, (2 * ns + 1) * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        TWG_CUDA(c, launch_scatter_tracks(src, c->d_track_off, ns, c->d_track_off + ns + 1, c->d_tracks, c->track_cap,
+                                          c->stream));
+        c->launches += 1;
     }
     // per-scenario params + cfg (pinned staging, one copy each)
     WarpCfgDev w;
@@ -308,8 +316,10 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     std::memcpy(hs + pbytes, &w, sizeof(w));
     TWG_CUDA(c, cudaMemcpyAsync(c->d_params, hs, pbytes, cudaMemcpyHostToDevice, c->stream));
     TWG_CUDA(c, cudaMemcpyAsync(c->d_wcfg, hs + pbytes, sizeof(w), cudaMemcpyHostToDevice, c->stream));
-    // clear warning flags of these scenarios
-    for (int k = 0; k < ns; ++k) TWG_CUDA(c, cudaMemsetAsync(c->d_flags + reqs[k].b, 0, sizeof(int), c->stream));
+    // clear warning flags of these scenarios (one memset when the call covers every scenario)
+    if (ns == c->B) TWG_CUDA(c, cudaMemsetAsync(c->d_flags, 0, c->B * sizeof(int), c->stream));
+    else
+        for (int k = 0; k < ns; ++k) TWG_CUDA(c, cudaMemsetAsync(c->d_flags + reqs[k].b, 0, sizeof(int), c->stream));
     EncodeArgs e;
     e.u0 = c->u[0];
     e.u1 = c->u[1];
@@ -625,7 +635,7 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
     void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_done,  c->d_sweeps, c->d_res_bits, c->d_res,
                     c->d_where,  c->d_cur,     c->d_flags, c->d_meta,  c->d_wcfg,   c->d_tracks,   c->d_t,
                     c->d_j,      c->d_pred,    c->d_boxes, c->d_params, c->d_track_off, c->d_cells, c->d_wp,
-                    c->d_smooth, c->d_idx};
+                    c->d_smooth, c->d_idx, c->d_track_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);

@@ -245,7 +245,7 @@ cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P,
 
 cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nscen, const int* scen_b, twg_track* dst,
                                   int cap, cudaStream_t st) {
-    k_scatter_tracks<<<dim3(4, nscen), 128, 0, st>>>(src, off, nscen, scen_b, dst, cap);
+    k_scatter_tracks<<<dim3(1, nscen), 128, 0, st>>>(src, off, nscen, scen_b, dst, cap);
     return cudaGetLastError();
 }
 

@@ -153,7 +153,9 @@ struct twg_ctx {
     twg::ScenParams* d_params = nullptr;
     int params_cap = 0;
     twg::WarpCfgDev* d_wcfg = nullptr;
-    int* d_track_off = nullptr;        // scatter offsets for device-side track input
+    int* d_track_off = nullptr;        // scatter offsets + scenario indices of one encode call
+    twg_track* d_track_tmp = nullptr;  // contiguous device copy of host track input
+    int64_t track_tmp_cap = 0;
     int track_off_cap = 0;
     // path buffers
     int path_len_cap = 0, smooth_cap = 0;
