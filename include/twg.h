@@ -249,6 +249,11 @@ TWG_API int64_t twg_kernel_launches(const twg_ctx* ctx);
 TWG_API twg_status twg_profile(twg_ctx* ctx, int32_t enable);
 TWG_API twg_status twg_profile_read(twg_ctx* ctx, double* relax_ms, int64_t* relax_launches, int64_t* cell_sweeps);
 
+/* Cycle accounting of the last descent walk of scenario b (performance
+ * debugging): out4 = {staging, chase, flush} in kilo-cycles of the walking
+ * thread, and the number of windows staged. */
+TWG_API twg_status twg_debug_walk(twg_ctx* ctx, int32_t b, int32_t* out4);
+
 /* Message of the last error on ctx ("" if none); ctx NULL: last twg_create error. */
 TWG_API const char* twg_last_error(const twg_ctx* ctx);
 

@@ -68,16 +68,16 @@ bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P, int 
     return r == CUDA_SUCCESS;
 }
 
-// The index matrix as {16 B, P / 16, H * B} uint8 with box {16, min(P, 512) / 16, 176}: one box
-// lands in shared memory as 176 rows of min(P, 512) contiguous bytes (k_walk windows).
-bool make_idx_map(CUtensorMap* m, uint8_t* base, int H, int B, int64_t P) {
+// The index matrix as a 2D {P, H * B} uint16 tensor with box {min(P, 256), 176}: one box lands in
+// shared memory as 176 rows of min(P, 256) contiguous descriptors (k_walk windows).
+bool make_idx_map(CUtensorMap* m, uint16_t* base, int H, int B, int64_t P) {
     auto enc = get_encode();
     if (!enc) return false;
-    cuuint64_t dims[3] = {16, (cuuint64_t)(P / 16), (cuuint64_t)H * (cuuint64_t)B};
-    cuuint64_t strides[2] = {16, (cuuint64_t)P};
-    cuuint32_t box[3] = {16, (cuuint32_t)(std::min<int64_t>(P, 512) / 16), 176};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)H * (cuuint64_t)B};
+    cuuint64_t strides[1] = {(cuuint64_t)P * 2};
+    cuuint32_t box[2] = {(cuuint32_t)std::min<int64_t>(P, 256), 176};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -411,6 +411,7 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
     TWG_CUDA(c, cudaMemcpyAsync(c->d_done, hs, B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     TWG_CUDA(c, cudaMemcpyAsync(c->d_cur, hs + B, B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     TWG_CUDA(c, cudaMemsetAsync(c->d_sweeps, 0, B * sizeof(int), c->stream));
+    TWG_CUDA(c, cudaMemsetAsync(c->d_where, 0xff, B * sizeof(int), c->stream));  // -1: not (yet) finished
     TWG_CUDA(c, cudaMemsetAsync(c->d_res_bits, 0, B * sizeof(unsigned), c->stream));
     TWG_CUDA(c, cudaMemsetAsync(c->d_res, 0, B * sizeof(float), c->stream));
     int nscen = 0;
@@ -480,8 +481,10 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
                 if (all) break;
             }
         }
-        TWG_CUDA(c, launch_fixup(c->u[0], c->u[1], c->sstride, B, c->d_where, c->d_cur, lp & 1, c->stream));
-        c->launches += 1;
+        if (tol > 0.0f) {  // only an early stop can leave a field in the other buffer
+            TWG_CUDA(c, launch_fixup(c->u[0], c->u[1], c->sstride, B, c->d_where, c->d_cur, lp & 1, c->stream));
+            c->launches += 1;
+        }
         for (int b = 0; b < B; ++b)
             if (part[b]) c->cur[b] ^= (lp & 1);
     }
@@ -547,6 +550,7 @@ twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg)
     p.smooth_cap = c->smooth_cap;
     p.meta = c->d_meta;
     p.idx = c->d_idx;
+    p.dir = c->d_dir;
     p.istride = c->sstride;
     p.idx_map = c->idx_map;
     int nl = 0;
@@ -609,9 +613,17 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     CK(dev_alloc(&c->d_flags, B));
     CK(dev_alloc(&c->d_meta, B));
     CK(dev_alloc(&c->d_idx, cells));
+    CK(dev_alloc(&c->d_dir, cells));
     CK(dev_alloc(&c->d_wcfg, 1));
     CK(cudaMemsetAsync(c->mask, 0, B * c->H * c->W, c->stream));
     CK(cudaMemsetAsync(c->d_meta, 0, B * sizeof(PathMeta), c->stream));
+    static bool preloaded = false;  // eager module loading (process-wide, once)
+    if (!preloaded) {
+        preload_relax_kernels();
+        preload_stamp_kernels();
+        preload_path_kernels();
+        preloaded = true;
+    }
     CK(launch_init_field(c->u[0], c->P, c->sstride, c->W, c->H, c->B, c->stream));
     CK(launch_init_field(c->u[1], c->P, c->sstride, c->W, c->H, c->B, c->stream));
     c->launches += 2;
@@ -635,7 +647,7 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
     void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_done,  c->d_sweeps, c->d_res_bits, c->d_res,
                     c->d_where,  c->d_cur,     c->d_flags, c->d_meta,  c->d_wcfg,   c->d_tracks,   c->d_t,
                     c->d_j,      c->d_pred,    c->d_boxes, c->d_params, c->d_track_off, c->d_cells, c->d_wp,
-                    c->d_smooth, c->d_idx, c->d_track_tmp};
+                    c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -860,6 +872,19 @@ TWG_API twg_status twg_field_ptr(twg_ctx* c, int32_t b, void** dev_ptr, int64_t*
     if (!c || b < 0 || b >= c->B) return TWG_E_INVALID_ARG;
     if (dev_ptr) *dev_ptr = c->u[c->cur[b]] + (int64_t)b * c->sstride;
     if (pitch) *pitch = c->P;
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_debug_walk(twg_ctx* c, int32_t b, int32_t* out4) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!out4 || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    PathMeta m;
+    TWG_CUDA(c, cudaMemcpy(&m, c->d_meta + b, sizeof(PathMeta), cudaMemcpyDeviceToHost));
+    out4[0] = m.pad[0];
+    out4[1] = m.pad[1];
+    out4[2] = m.pad[2] & 0xfffff;
+    out4[3] = m.pad[2] >> 20;
     return TWG_OK;
 }
 

@@ -231,7 +231,7 @@ __global__ void k_fixup(float* __restrict__ u0, float* __restrict__ u1, int64_t 
                         const int* __restrict__ cur, int lp) {
     const int b = blockIdx.y;
     const int tgt = cur[b] ^ lp;
-    if (where[b] == tgt) return;
+    if (where[b] < 0 || where[b] == tgt) return;  // not relaxed in this call, or already in place
     const float4* src = reinterpret_cast<const float4*>((tgt ? u0 : u1) + (int64_t)b * sstride);
     float4* dst = reinterpret_cast<float4*>((tgt ? u1 : u0) + (int64_t)b * sstride);
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < sstride / 4; q += (int64_t)gridDim.x * blockDim.x)
@@ -274,6 +274,27 @@ cudaError_t launch_rb_tblock(int T, const CUtensorMap& m0, const CUtensorMap& m1
         case 8: return launch_T3<8>(m0, m1, a, B, qoff, resid, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// Force module loading of every relaxation kernel instance (CUDA lazy loading would otherwise put a
+// millisecond-scale load inside the first launch of each instance).
+template <int T>
+static void preload_T() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, k_rb_tblock<T, 0, false>);
+    cudaFuncGetAttributes(&a, k_rb_tblock<T, 0, true>);
+    cudaFuncGetAttributes(&a, k_rb_tblock<T, 1, false>);
+    cudaFuncGetAttributes(&a, k_rb_tblock<T, 1, true>);
+}
+
+void preload_relax_kernels() {
+    preload_T<1>(); preload_T<2>(); preload_T<3>(); preload_T<4>();
+    preload_T<5>(); preload_T<6>(); preload_T<7>(); preload_T<8>();
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, k_rb_simple);
+    cudaFuncGetAttributes(&a, k_check);
+    cudaFuncGetAttributes(&a, k_fixup);
+    cudaGetLastError();
 }
 
 cudaError_t launch_rb_simple(float* u, int64_t P, int64_t sstride, int W, int H, int B, int color, int row_off,

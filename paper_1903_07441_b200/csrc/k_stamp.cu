@@ -249,6 +249,20 @@ cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nsce
     return cudaGetLastError();
 }
 
+void preload_stamp_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, k_encode_cold);
+    cudaFuncGetAttributes(&a, k_unstamp);
+    cudaFuncGetAttributes(&a, k_goal_reset);
+    cudaFuncGetAttributes(&a, k_track_predict);
+    cudaFuncGetAttributes(&a, k_stamp);
+    cudaFuncGetAttributes(&a, k_set_goal);
+    cudaFuncGetAttributes(&a, k_scatter_tracks);
+    cudaFuncGetAttributes(&a, k_convert);
+    cudaFuncGetAttributes(&a, k_import);
+    cudaGetLastError();
+}
+
 cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_tracks, int any_cold, int* n_launch,
                           cudaStream_t st) {
     int nl = 0;

@@ -105,6 +105,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -163,7 +170,8 @@ struct twg_ctx {
     float2* d_wp = nullptr;            // [B][path_len_cap]
     float2* d_smooth = nullptr;        // [B][smooth_cap]
     twg::PathMeta* d_meta = nullptr;   // [B]
-    uint8_t* d_idx = nullptr;          // index matrix [B][H][P] bytes
+    uint16_t* d_idx = nullptr;         // index matrix (4-step descriptors) [B][H][P]
+    uint8_t* d_dir = nullptr;          // index matrix (direction bytes) [B][H][P]
     CUtensorMap idx_map;               // TMA view of d_idx for the walker's windows
     // pinned host staging
     void* h_stage = nullptr;

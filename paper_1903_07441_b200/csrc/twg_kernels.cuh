@@ -56,10 +56,16 @@ struct PathArgs {
     float2* smooth;        // [B][smooth_cap]
     int len_cap, smooth_cap;
     PathMeta* meta;        // [B]
-    uint8_t* idx;          // index matrix M_idx, [B][H][P] bytes (Eq. 3)
-    int64_t istride;       // bytes per scenario (H * P)
-    CUtensorMap idx_map;   // M_idx viewed as {16, P / 16, H * B} bytes, box {16, min(P, 512) / 16, 176}
+    uint16_t* idx;         // index matrix M_idx as 4-step descriptors, [B][H][P] (Eq. 3)
+    uint8_t* dir;          // index matrix M_idx as one direction byte per cell, [B][H][P]
+    int64_t istride;       // entries per scenario (H * P)
+    CUtensorMap idx_map;   // M_idx viewed as {8, P / 8, H * B} uint16, box {8, min(P, 256) / 8, 176}
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
+
+// Module preloading (called once by twg_create)
+void preload_relax_kernels();
+void preload_stamp_kernels();
+void preload_path_kernels();
 
 }  // namespace twg

@@ -72,6 +72,7 @@ SIGNATURES = [
     ("twg_set_field", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_get_warp", C.c_int32, [_P, C.c_int32, C.c_int32, _P, _P, _P]),
     ("twg_field_ptr", C.c_int32, [_P, C.c_int32, C.POINTER(_P), C.POINTER(C.c_int64)]),
+    ("twg_debug_walk", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_kernel_launches", C.c_int64, [_P]),
     ("twg_profile", C.c_int32, [_P, C.c_int32]),
     ("twg_profile_read", C.c_int32, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -245,6 +246,11 @@ class Planner:
         pitch = C.c_int64()
         _check(self.ctx, lib().twg_field_ptr(self.ctx, b, C.byref(p), C.byref(pitch)))
         return p.value, pitch.value
+
+    def debug_walk(self, b=0):
+        out = np.zeros(4, np.int32)
+        _check(self.ctx, lib().twg_debug_walk(self.ctx, b, _ptr(out)))
+        return {"stage_kcyc": int(out[0]), "chase_kcyc": int(out[1]), "flush_kcyc": int(out[2]), "windows": int(out[3])}
 
     def kernel_launches(self):
         return int(lib().twg_kernel_launches(self.ctx))

@@ -281,3 +281,20 @@ def test_c3_full_size_fixed_budget():
     assert st == ref["walk_status"]
     if st == T.OK:
         assert np.array_equal(cells, ref["cells"])
+
+
+def test_single_scenario_relax_leaves_others_bitwise_untouched():
+    """twg_plan_step(b) relaxes scenario b only; with an odd number of launches and an early stop
+    the other scenarios' fields must not move (regression: stale per-scenario buffer indices)."""
+    scs = [scene_c2(s) for s in range(3)]
+    pl = Planner(512, 512, 3, 0.1, (0.0, 0.0), device=0, stream=_stream())
+    for b, sc in enumerate(scs):
+        pl.set_static(sc.static, b)
+        pl.set_obstacles(b, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
+    pl.relax(relax_cfg(max_sweeps=7, temporal_depth=3))
+    before = [pl.get_field(b, 0).copy() for b in range(3)]
+    for sweeps, T_, tol in ((5, 2, 0.0), (9, 3, 0.0), (40, 4, 1e-2)):
+        pl.plan_step(1, [scs[1].robot], [scs[1].goal], scs[1].tracks, [scs[1].n_tracks], warp_cfg(),
+                     relax_cfg(max_sweeps=sweeps, check_every=4, tol=tol, temporal_depth=T_), band_cfg(5, 3000, 6000))
+        for b in (0, 2):
+            assert np.array_equal(pl.get_field(b, 0).view(np.uint32), before[b].view(np.uint32))

@@ -16,6 +16,7 @@ for it in (0, 50, 50, 50):
     torch.cuda.synchronize(); t1 = time.time()
     s, cells, sm, ns, nxt = pl.extract_path(0, band_cfg(it, 40000, 80000))
     torch.cuda.synchronize(); t2 = time.time()
-    print(json.dumps({"iters": it, "walk": s, "n_cells": len(cells), "n_smooth": int(ns), "ms": 1e3 * (t2 - t1)}), flush=True)
+    print(json.dumps({"iters": it, "walk": s, "n_cells": len(cells), "n_smooth": int(ns), "ms": 1e3 * (t2 - t1),
+                      **pl.debug_walk(0)}), flush=True)
 if len(sys.argv) > 1:
     np.save(sys.argv[1], pl.get_field(0, 0))
