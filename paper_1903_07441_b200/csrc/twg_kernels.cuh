@@ -58,8 +58,9 @@ struct PathArgs {
     PathMeta* meta;        // [B]
     uint16_t* idx;         // index matrix M_idx as 4-step descriptors, [B][H][P] (Eq. 3)
     uint8_t* dir;          // index matrix M_idx as one direction byte per cell, [B][H][P]
+    int win_pitch;         // walker window row pitch (cells) = 256; descriptor offsets use it
     int64_t istride;       // entries per scenario (H * P)
-    CUtensorMap idx_map;   // M_idx viewed as {8, P / 8, H * B} uint16, box {8, min(P, 256) / 8, 176}
+    CUtensorMap idx_map;   // M_idx as a 2D {P, H * B} uint16 tensor, box {256, 176}
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
 
