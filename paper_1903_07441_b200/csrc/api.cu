@@ -435,10 +435,11 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
         int done_sw = 0, nchunk = 0;
         while (done_sw < maxs) {
             const int chunk = std::min(check, maxs - done_sw);
-            // launches of T sweeps; the remainder first; the last launch accumulates the residual
+            // launches of T sweeps, then the remainder; the last launch accumulates the residual (the
+            // tracking costs the most in the deepest kernel, so a short remainder launch carries it)
             std::vector<int> plan;
-            if (chunk % T) plan.push_back(chunk % T);
             for (int q = 0; q < chunk / T; ++q) plan.push_back(T);
+            if (chunk % T) plan.push_back(chunk % T);
             for (size_t q = 0; q < plan.size(); ++q) {
                 const int t = plan[q];
                 a.n_strips = (c->W + out_cols(t) - 1) / out_cols(t);
