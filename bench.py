@@ -274,6 +274,10 @@ def run_ours(args):
     T_eff = rcells / rl / cells if rl else 0
     bytes_per_launch = 8.0 * cells  # one fp32 read + one fp32 write per cell per launch
     achieved = bytes_per_launch / avg_launch_s / 1e9
+    traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum of one launch, from the committed ncu capture
+    tp = os.path.join(ROOT, "profiles", "r01_relax_traffic.json")
+    if os.path.exists(tp) and N == 4096:
+        traffic = json.load(open(tp)).get("traffic_bytes_per_launch")
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -286,7 +290,7 @@ def run_ours(args):
         "plan_steps_per_s": args.steps * ws / (ms * 1e-3),
         "relax_glups": cells * args.relax_sweeps / (relax_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "k_rb_tblock", "bytes_per_launch": bytes_per_launch,
+                     "traffic": traffic, "kernel": "k_rb_tblock", "bytes_per_launch": bytes_per_launch,
                      "sweeps_per_launch": T_eff, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,
                      "effective_glups_vs_8B_per_LUP": (rcells / (rms * 1e-3) / 1e9) / (peak / 8.0) if rms else None},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(sc0.n_tracks * 160 + 40),
