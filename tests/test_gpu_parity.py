@@ -298,3 +298,93 @@ def test_single_scenario_relax_leaves_others_bitwise_untouched():
                      relax_cfg(max_sweeps=sweeps, check_every=4, tol=tol, temporal_depth=T_), band_cfg(5, 3000, 6000))
         for b in (0, 2):
             assert np.array_equal(pl.get_field(b, 0).view(np.uint32), before[b].view(np.uint32))
+
+
+# ------------------------------------------------------------------ degenerate cases
+def test_start_equals_goal_and_zero_band_iterations():
+    from scenes.gen import Scene
+    from scenes import default_warp_cfg
+    N = 40
+    static = np.zeros((N, N), np.uint8)
+    sc = Scene("sg", N, N, 0.1, (0.0, 0.0), static, (2.05, 2.05, 0.0, 0.4), (20, 20), np.zeros((0, 20)),
+               default_warp_cfg(), 0)
+    pl = _planner(sc)
+    pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
+    pl.relax(relax_cfg(max_sweeps=50))
+    st, cells, smooth, ns, nxt = pl.extract_path(0, band_cfg(50, 100, 200))
+    assert st == T.OK and cells.tolist() == [[20, 20]] and ns == 1 and np.allclose(smooth, [[20.5, 20.5]])
+    assert nxt == (20.5, 20.5)
+    sc2 = Scene("sg2", N, N, 0.1, (0.0, 0.0), static, (0.55, 0.55, 0.0, 0.4), (30, 33), np.zeros((0, 20)),
+                default_warp_cfg(), 0)
+    pl2 = _planner(sc2)
+    pl2.set_obstacles(0, sc2.robot, sc2.goal, sc2.tracks, warp_cfg(), warm=0)
+    pl2.relax(relax_cfg(max_sweeps=4000))
+    st, cells, smooth, ns, nxt = pl2.extract_path(0, band_cfg(0, 400, 800))
+    ref = oracle.plan_step(sc2, max_sweeps=4000, iters=0, max_len=400)
+    assert np.array_equal(cells, ref["cells"]) and np.array_equal(smooth, ref["smooth"])
+
+
+def test_goal_less_field_relaxes_to_zero_and_walk_fails():
+    """No goal reachable (the goal is walled in): free cells decay towards u = 0, the walk reports NoPath."""
+    from scenes.gen import Scene
+    from scenes import default_warp_cfg
+    N = 48
+    static = np.zeros((N, N), np.uint8)
+    static[20:29, 20] = 1; static[20:29, 28] = 1; static[20, 20:29] = 1; static[28, 20:29] = 1
+    sc = Scene("gl", N, N, 0.1, (0.0, 0.0), static, (0.55, 0.55, 0.0, 0.4), (24, 24), np.zeros((0, 20)),
+               default_warp_cfg(), 0)
+    pl = _planner(sc)
+    pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
+    sw, res = pl.relax(relax_cfg(max_sweeps=3000, temporal_depth=5))
+    ref = oracle.plan_step(sc, max_sweeps=3000, iters=5, max_len=3000)
+    _assert_field(pl.get_field(0, 1), ref["u"])
+    st, cells, *_ = pl.extract_path(0, band_cfg(5, 3000, 6000))
+    assert st == T.E_NO_PATH == ref["walk_status"]
+
+
+# ------------------------------------------------------------------ full sizes of BASELINE configs 4 and 5
+@pytest.mark.slow
+def test_c4_full_size_sampled_rows():
+    """16384^2 (BASELINE configs[3]) on one GPU: 8 sweeps in the default launch configuration; the
+    oracle relaxes row bands independently (a band of R rows plus 2 * 8 rows of context is exact
+    for 8 sweeps) and the sampled rows must match bit for bit."""
+    from scenes import scene_c4
+    sc = scene_c4(0)
+    pl = _planner(sc)
+    pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
+    S = 8
+    pl.relax(relax_cfg(max_sweeps=S))
+    raw = pl.get_field(0, 0)
+    st, cls, *_ = oracle.classify(sc)
+    assert np.array_equal(_classes_from_raw(raw), cls)
+    for r0 in (0, 5000, 16384 - 40):
+        lo, hi = max(r0 - 2 * S, 0), min(r0 + 40 + 2 * S, sc.H)
+        sub_cls = np.ascontiguousarray(cls[lo:hi])
+        # rows outside the band act as walls only where the band ends inside the grid: their
+        # influence reaches at most 2S rows in, which the context absorbs
+        u = oracle.init_u32(sub_cls)
+        oracle.relax_f32_ex(sub_cls, u, S, S, 0.0, row_parity=lo)
+        assert np.array_equal(np.abs(raw[r0:r0 + 40]), u[r0 - lo:r0 - lo + 40])
+
+
+@pytest.mark.slow
+def test_c5_full_batch_sampled_scenarios():
+    """1024 x 512^2 (BASELINE configs[4]) in one batched context: a cold plan step with S = 100
+    for all scenarios; 6 sampled scenarios are replayed by the oracle."""
+    from scenes import scene_c5
+    scs = scene_c5(1024)
+    pl = Planner(512, 512, 1024, 0.1, (0.0, 0.0), device=0, stream=_stream())
+    for b, sc in enumerate(scs):
+        pl.set_static(sc.static, b)
+    tracks = np.vstack([sc.tracks for sc in scs])
+    bc = band_cfg(50, 2048, 4096)
+    st, res, cells, sm = pl.plan_step(-1, [sc.robot for sc in scs], [sc.goal for sc in scs], tracks,
+                                      [sc.n_tracks for sc in scs], warp_cfg(), relax_cfg(max_sweeps=100, warm_start=0),
+                                      bc)
+    for b in (0, 1, 313, 512, 777, 1023):
+        ref = oracle.plan_step(scs[b], max_sweeps=100, iters=50, max_len=2048)
+        _assert_field(pl.get_field(b, 1), ref["u"])
+        assert res[b].walk_status == ref["walk_status"] and res[b].sweeps == 100
+        if ref["walk_status"] == 0:
+            assert np.array_equal(cells[b, : res[b].n_cells], ref["cells"])
+            assert np.abs(sm[b, : res[b].n_smooth] - ref["smooth"]).max() <= 1e-4
