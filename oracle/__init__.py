@@ -66,7 +66,15 @@ def lib():
         L.orc_stamp_box.argtypes = [i32, i32, d, d, d, d, d, d, P]
         L.orc_classify.restype = i32
         L.orc_classify.argtypes = [i32, i32, d, d, d, P, i32, i32, d, d, d, d, i32, P,
-                                   d, P, d, d, d, i32, P, P, P, P]
+                                   d, P, d, d, d, i32, i32, i32, P, P, P, P]
+        L.orc_horizon_ring.restype = i32
+        L.orc_horizon_ring.argtypes = [i32, d, d, d, i32]
+        L.orc_relax_jacobi_f32.restype = i32
+        L.orc_relax_jacobi_f32.argtypes = [i32, i32, P, P, i32, i32, f32, P]
+        L.orc_index_matrix.restype = None
+        L.orc_index_matrix.argtypes = [i32, i32, P, P, P]
+        L.orc_warp_map.restype = None
+        L.orc_warp_map.argtypes = [i32, i32, d, d, d, d, d, d, d, P]
         L.orc_init_u32.restype = None
         L.orc_init_u32.argtypes = [i64, P, P, P]
         L.orc_init_u64.restype = None
@@ -116,6 +124,10 @@ def horizon(t, speed_r, vx, vy, eps_v=0.05, hmax=20):
     return lib().orc_horizon(t, speed_r, vx, vy, eps_v, hmax)
 
 
+def horizon_ring(t, w, speed_r, dt, hmax=20):
+    return lib().orc_horizon_ring(t, w, speed_r, dt, hmax)
+
+
 def predict(x, P, Q, dt, j):
     x = np.ascontiguousarray(x, np.float64).reshape(4)
     P = np.ascontiguousarray(P, np.float64).reshape(16)
@@ -139,7 +151,7 @@ def stamp_disk(W, H, cs, ox, oy, xp, yp, R2, brute=True):
 
 
 # ---------------------------------------------------------------- O3
-def classify(scene):
+def classify(scene, horizon_mode=0, footprint_mode=0):
     """Class grid (uint8 H x W: 0 free, 1 obstacle, 2 goal) plus per-track t, j, (xp, yp, R2)."""
     W, H = scene.W, scene.H
     static = np.ascontiguousarray(scene.static, np.uint8)
@@ -155,7 +167,8 @@ def classify(scene):
     st = lib().orc_classify(W, H, scene.cell_size, scene.origin[0], scene.origin[1], _p(static),
                             int(scene.goal[0]), int(scene.goal[1]), xr, yr, th, sp,
                             n, _p(tracks), wc.dt, _p(Q), wc.warp_spacing, wc.eps_v,
-                            wc.safety_radius, int(wc.horizon_max), _p(cls), _p(t), _p(j), _p(pred))
+                            wc.safety_radius, int(wc.horizon_max), int(horizon_mode), int(footprint_mode),
+                            _p(cls), _p(t), _p(j), _p(pred))
     return st, cls, t[:n], j[:n], pred[:n]
 
 
@@ -216,6 +229,32 @@ def relax_f64(cls, u, max_sweeps, check_every=1, tol=0.0):
     return int(s), float(r[0])
 
 
+def relax_jacobi_f32(cls, u, max_sweeps, check_every=1, tol=0.0):
+    assert u.dtype == np.float32 and u.flags.c_contiguous
+    cls = np.ascontiguousarray(cls, np.uint8)
+    H, W = u.shape
+    r = np.zeros(1, np.float32)
+    s = lib().orc_relax_jacobi_f32(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol), _p(r))
+    return int(s), float(r[0])
+
+
+def index_matrix(cls, u):
+    cls = np.ascontiguousarray(cls, np.uint8)
+    u = np.ascontiguousarray(u, np.float32)
+    out = np.zeros(u.shape, np.uint8)
+    H, W = u.shape
+    lib().orc_index_matrix(W, H, _p(cls), _p(u), _p(out))
+    return out
+
+
+def warp_map(scene):
+    out = np.zeros((scene.H, scene.W), np.int32)
+    xr, yr, th, _ = scene.robot
+    lib().orc_warp_map(scene.W, scene.H, scene.cell_size, scene.origin[0], scene.origin[1], xr, yr, th,
+                       scene.warp.warp_spacing, _p(out))
+    return out
+
+
 def jacobi_f64(cls, u, max_sweeps, tol=0.0):
     assert u.dtype == np.float64 and u.flags.c_contiguous
     cls = np.ascontiguousarray(cls, np.uint8)
@@ -274,21 +313,22 @@ def next_waypoint(pts):
 
 
 def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0.25, kt=1.0,
-              max_len=None, prev=None):
+              max_len=None, prev=None, jacobi=False, horizon_mode=0, footprint_mode=0):
     """One planning tick, Algorithm 1 on the CPU.
 
     prev: None (cold start) or the dict returned by the previous call (warm
     start, C7).  Returns a dict with class grid, field (float32 u), sweeps,
     residual, walk status/cells, smoothed path and next waypoint.
     """
-    st, cls, t, j, pred = classify(scene)
+    st, cls, t, j, pred = classify(scene, horizon_mode, footprint_mode)
     if st < 0:
         return {"status": st}
     if prev is None:
         u = init_u32(cls)
     else:
         u = init_u32(cls, prev["u"])
-    sweeps, res = relax_f32(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol)
+    relax = relax_jacobi_f32 if jacobi else relax_f32
+    sweeps, res = relax(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol)
     if max_len is None:
         max_len = 4 * (scene.W + scene.H)
     wst, cells = walk(cls, u, robot_cell(scene), max_len)

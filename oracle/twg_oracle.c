@@ -93,6 +93,20 @@ int32_t orc_horizon(int32_t t, double speed_r, double vx, double vy, double eps_
     return (int32_t)j;
 }
 
+/* Alternative horizon reading (north_star "the time the robot needs to reach that
+ * grid ring"): ring t lies ~ t w metres away, reached after t w / speed_r seconds, i.e.
+ * j = clamp(round(t w / (speed_r dt)), 0, horizon_max) Kalman steps (speed_r <= 0: horizon_max). */
+int32_t orc_horizon_ring(int32_t t, double w, double speed_r, double dt, int32_t hmax)
+{
+    if (!(speed_r > 0.0)) return hmax;
+    double steps = ((double)t * w) / (speed_r * dt);
+    if (!(steps < 4.0e18)) return hmax;
+    long long j = llround(steps);
+    if (j < 0) j = 0;
+    if (j > hmax) j = hmax;
+    return (int32_t)j;
+}
+
 /* A of P:548-553: constant velocity, dt in the (0,2) and (1,3) slots. */
 static void orc_A(double dt, double A[16])
 {
@@ -194,11 +208,15 @@ void orc_stamp_box(int32_t W, int32_t H, double cs, double ox, double oy,
     orc_stamp_one(W, H, cs, ox, oy, xp, yp, R2, stamp, 1);
 }
 
+/* horizon_mode 0: Eq. 16 (C18); 1: time to reach the ring (orc_horizon_ring, f4).
+ * footprint_mode 0: the j-step predicted covariance (C19); 1: the track's posterior covariance
+ * P_k|k ("uncertainty given by Kalman filter at each step (Equation 12)", f4). */
 int32_t orc_classify(int32_t W, int32_t H, double cs, double ox, double oy,
                      const uint8_t* static_mask, int32_t gx, int32_t gy,
                      double xr, double yr, double theta, double speed,
                      int32_t n, const double* tracks,
                      double dt, const double* Q, double w, double eps_v, double rs, int32_t hmax,
+                     int32_t horizon_mode, int32_t footprint_mode,
                      uint8_t* cls, int32_t* t_out, int32_t* j_out, double* pred_out)
 {
     if (W <= 0 || H <= 0 || cs <= 0.0 || n < 0) return ORC_E_INVALID_ARG;
@@ -220,10 +238,11 @@ int32_t orc_classify(int32_t W, int32_t H, double cs, double ox, double oy,
         const double* P = x + 4;
         double rx = orc_warp_radius(xr, yr, c, s, x[0], x[1]);      /* O1, C24: from x_hat */
         int32_t t = orc_warp_number(rx, w);
-        int32_t j = orc_horizon(t, speed, x[2], x[3], eps_v, hmax);  /* O2 */
+        int32_t j = horizon_mode == 1 ? orc_horizon_ring(t, w, speed, dt, hmax)
+                                       : orc_horizon(t, speed, x[2], x[3], eps_v, hmax);  /* O2 */
         double xo[4], Po[16];
         orc_predict(x, P, Q, dt, j, xo, Po);
-        double R2 = orc_footprint_r2(Po, rs);
+        double R2 = orc_footprint_r2(footprint_mode == 1 ? P : Po, rs);
         if (t_out) t_out[i] = t;
         if (j_out) j_out[i] = j;
         if (pred_out) { pred_out[3 * i] = xo[0]; pred_out[3 * i + 1] = xo[1]; pred_out[3 * i + 2] = R2; }
@@ -376,6 +395,77 @@ int32_t orc_jacobi_f64(int32_t W, int32_t H, const uint8_t* cls, double* u,
     free(old);
     if (res_out) *res_out = res;
     return s;
+}
+
+/* Jacobi, Eq. 1 literally, in fp32: every free cell from the previous
+ * iterate, 0.25 * ((E + W) + (N + S)); residual and stop rule as orc_relax_f32. */
+int32_t orc_relax_jacobi_f32(int32_t W, int32_t H, const uint8_t* cls, float* u, int32_t max_sweeps,
+                             int32_t check_every, float tol, float* res_out)
+{
+    size_t ncell = (size_t)W * H;
+    float* old = (float*)malloc(ncell * sizeof(float));
+    float res = 0.0f;
+    int32_t s = 0;
+    if (check_every < 1) check_every = 1;
+    for (s = 1; s <= max_sweeps; ++s) {
+        memcpy(old, u, ncell * sizeof(float));
+        res = 0.0f;
+        for (int32_t y = 0; y < H; ++y)
+            for (int32_t x = 0; x < W; ++x) {
+                size_t q = (size_t)y * W + x;
+                if (cls[q] != ORC_FREE) continue;
+                float uE = x + 1 < W ? old[q + 1] : 0.0f;
+                float uW = x > 0 ? old[q - 1] : 0.0f;
+                float uN = y > 0 ? old[q - W] : 0.0f;
+                float uS = y + 1 < H ? old[q + W] : 0.0f;
+                float nv = 0.25f * ((uE + uW) + (uN + uS));
+                float d = fabsf(nv - old[q]);
+                if (d > res) res = d;
+                u[q] = nv;
+            }
+        if ((s % check_every == 0 && res < tol) || s == max_sweeps) break;
+    }
+    if (max_sweeps <= 0) { s = 0; res = 0.0f; }
+    free(old);
+    if (res_out) *res_out = res;
+    return s;
+}
+
+/* Full-grid index matrix M_idx (Eq. 3; Alg. 1): per cell
+ * 0..3 = the in-grid neighbour with the largest u in the order +x, -x, +y, -y (strict >), or
+ * 4 goal, 5 obstacle, 6 no in-grid neighbour. */
+void orc_index_matrix(int32_t W, int32_t H, const uint8_t* cls, const float* u, uint8_t* out)
+{
+    static const int dxs[4] = { +1, -1, 0, 0 };
+    static const int dys[4] = { 0, 0, +1, -1 };
+    for (int32_t y = 0; y < H; ++y)
+        for (int32_t x = 0; x < W; ++x) {
+            size_t q = (size_t)y * W + x;
+            if (cls[q] == ORC_GOAL) { out[q] = 4; continue; }
+            if (cls[q] == ORC_OBSTACLE) { out[q] = 5; continue; }
+            int best_d = 6;
+            float best = 0.0f;
+            for (int d = 0; d < 4; ++d) {
+                int nx = x + dxs[d], ny = y + dys[d];
+                if (nx < 0 || ny < 0 || nx >= W || ny >= H) continue;
+                float v = u[(size_t)ny * W + nx];
+                if (best_d == 6 || v > best) { best = v; best_d = d; }
+            }
+            out[q] = (uint8_t)best_d;
+        }
+}
+
+/* Per-cell warp number (the paper's kernel 1, "calculate the warp of each cell"; the
+ * numbered ellipses of Fig. warps): t of an obstacle at the cell centre. */
+void orc_warp_map(int32_t W, int32_t H, double cs, double ox, double oy, double xr, double yr, double theta,
+                  double w, int32_t* out)
+{
+    double c = cos(theta), s = sin(theta);
+    for (int32_t y = 0; y < H; ++y)
+        for (int32_t x = 0; x < W; ++x) {
+            double px = ox + ((double)x + 0.5) * cs, py = oy + ((double)y + 0.5) * cs;
+            out[(size_t)y * W + x] = orc_warp_number(orc_warp_radius(xr, yr, c, s, px, py), w);
+        }
 }
 
 /* ------------------------------------------------------------------------ */
