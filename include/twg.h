@@ -103,7 +103,12 @@ typedef struct {
  *   dt [0.1 s] Kalman step; Q [1e-3 diag(dt^4/4, dt^4/4, dt^2, dt^2), S:307]
  *   process noise, row-major; warp_spacing [1.0 m] width of one warp ring
  *   (C17); eps_v [0.05 m/s] obstacle-speed floor of Eq. 16 (C18);
- *   safety_radius [0.5 m] (C20); horizon_max [20] clamp of j (C18). */
+ *   safety_radius [0.5 m] (C20); horizon_max [20] clamp of j (C18);
+ *   horizon_mode [0]: 0 = Eq. 16, j = round(v t), v = speed ratio (C18);
+ *     1 = time the robot needs to reach ring t, j = round(t w / (speed_r dt))
+ *     (north_star wording; C26);
+ *   footprint_mode [0]: 0 = covariance after the j predicts (C19);
+ *     1 = the track's own posterior covariance P_k|k (C27). */
 typedef struct {
     double dt;
     double Q[16];
@@ -111,6 +116,8 @@ typedef struct {
     double eps_v;
     double safety_radius;
     int32_t horizon_max;
+    int32_t horizon_mode;
+    int32_t footprint_mode;
     int32_t reserved;
 } twg_warp_cfg;
 
@@ -123,11 +130,14 @@ typedef struct {
  *   rows_per_warp [0 = auto, load model of DESIGN.md]: rows of the strip one
  *   warp owns;
  *   sync_every [64]: convergence flags are read back every sync_every
- *   checks when tol > 0. */
+ *   checks when tol > 0;
+ *   mode [0]: 0 = red-black Gauss-Seidel (Eq. 2, the hot path);
+ *   1 = Jacobi (Eq. 1: every free cell from the previous iterate;
+ *   temporal_depth and rows_per_warp ignored). */
 typedef struct {
     int32_t max_sweeps, check_every, warm_start, temporal_depth;
     float tol;
-    int32_t rows_per_warp, sync_every, reserved;
+    int32_t rows_per_warp, sync_every, mode;
 } twg_relax_cfg;
 
 /* Path output control (rows a7-a9):
@@ -236,6 +246,23 @@ TWG_API twg_status twg_set_field(twg_ctx* ctx, int32_t b, const float* raw);
  * for parity tests): t[n] warp numbers, j[n] horizons, pred[3 n] =
  * (x_pred, y_pred, R^2).  n must equal the track count of that call. */
 TWG_API twg_status twg_get_warp(twg_ctx* ctx, int32_t b, int32_t n, int32_t* t, int32_t* j, double* pred);
+
+/* Full-grid index matrix M_idx of scenario b's current field (Eq. 3,
+ * P:228-233; Alg. 1): out[height x width] uint8
+ * row-major (host or device): 0..3 = step to the in-grid neighbour with the
+ * largest u, order +x, -x, +y, -y, first maximum wins (C8); 4 goal;
+ * 5 obstacle; 6 no in-grid neighbour (1 x 1 grid).  Cells on a slab's
+ * ghost rows use the local grid only.  Errors: INVALID_ARG, CUDA. */
+TWG_API twg_status twg_index_matrix(twg_ctx* ctx, int32_t b, uint8_t* out);
+
+/* Per-cell warp number (the paper's kernel 1, "calculate the warp
+ * of each cell"; the numbered ellipses of P:438-456):
+ * out[height x width] int32 row-major (host or device), t = max(1,
+ * ceil(r_x / warp_spacing)) of an obstacle at the cell centre (C16, C17)
+ * for the robot pose `robot` on this context's grid geometry (origin,
+ * cell_size; a slab's local rows).  Errors: INVALID_ARG
+ * (warp_spacing <= 0), CUDA. */
+TWG_API twg_status twg_warp_map(twg_ctx* ctx, const twg_robot* robot, double warp_spacing, int32_t* out);
 
 /* Device pointer and pitch (floats) of scenario b's current field buffer
  * (valid until the next call on ctx). */

@@ -224,6 +224,8 @@ twg_status validate(twg_ctx* c, const EncodeReq& r, int* rcx, int* rcy) {
 twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_track* tracks, const twg_warp_cfg* wc,
                   int warm_req) {
     if (!wc) return fail(c, TWG_E_INVALID_ARG, "null warp cfg");
+    if ((wc->horizon_mode != 0 && wc->horizon_mode != 1) || (wc->footprint_mode != 0 && wc->footprint_mode != 1))
+        return fail(c, TWG_E_INVALID_ARG, "horizon_mode / footprint_mode must be 0 or 1");
     const int ns = (int)reqs.size();
     std::vector<ScenParams> ps(ns);
     int max_n = 0, max_prev = 0, any_cold = 0;
@@ -309,6 +311,8 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     w.eps_v = wc->eps_v;
     w.rs = wc->safety_radius;
     w.hmax = wc->horizon_max;
+    w.hmode = wc->horizon_mode;
+    w.fmode = wc->footprint_mode;
     const size_t pbytes = ns * sizeof(ScenParams);
     char* hs = nullptr;
     TWG_CUDA(c, stage_alloc(c, pbytes + sizeof(WarpCfgDev) + 64, reinterpret_cast<void**>(&hs)));
@@ -396,6 +400,8 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
     if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null relax cfg");
     const int maxs = cfg->max_sweeps;
     if (maxs < 0 || cfg->check_every < 0) return fail(c, TWG_E_INVALID_ARG, "negative sweep counts");
+    if (cfg->mode != 0 && cfg->mode != 1) return fail(c, TWG_E_INVALID_ARG, "relax mode must be 0 or 1");
+    const bool jacobi = cfg->mode == 1;
     const int B = c->B;
     int T = cfg->temporal_depth > 0 ? std::min(cfg->temporal_depth, kMaxT) : 6;
     const float tol = cfg->tol;
@@ -438,8 +444,12 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
             // launches of T sweeps, then the remainder; the last launch accumulates the residual (the
             // tracking costs the most in the deepest kernel, so a short remainder launch carries it)
             std::vector<int> plan;
-            for (int q = 0; q < chunk / T; ++q) plan.push_back(T);
-            if (chunk % T) plan.push_back(chunk % T);
+            if (jacobi) {
+                plan.assign(chunk, 1);
+            } else {
+                for (int q = 0; q < chunk / T; ++q) plan.push_back(T);
+                if (chunk % T) plan.push_back(chunk % T);
+            }
             for (size_t q = 0; q < plan.size(); ++q) {
                 const int t = plan[q];
                 a.n_strips = (c->W + out_cols(t) - 1) / out_cols(t);
@@ -458,7 +468,11 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
                     e1 = c->ev_pool[c->ev_used++];
                     TWG_CUDA(c, cudaEventRecord(e0, c->stream));
                 }
-                TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0][t], c->tmap[1][t], a, B, qoff, q + 1 == plan.size(), c->stream));
+                if (jacobi)
+                    TWG_CUDA(c, launch_jacobi(a, B, q + 1 == plan.size(), c->stream));
+                else
+                    TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0][t], c->tmap[1][t], a, B, qoff, q + 1 == plan.size(),
+                                                 c->stream));
                 if (c->prof) {
                     TWG_CUDA(c, cudaEventRecord(e1, c->stream));
                     c->prof_launches += 1;
@@ -866,6 +880,60 @@ TWG_API twg_status twg_get_warp(twg_ctx* c, int32_t b, int32_t n, int32_t* t, in
     if (t) TWG_CUDA(c, cudaMemcpyAsync(t, c->d_t + o, n * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (j) TWG_CUDA(c, cudaMemcpyAsync(j, c->d_j + o, n * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (pred) TWG_CUDA(c, cudaMemcpyAsync(pred, c->d_pred + 3 * o, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_index_matrix(twg_ctx* c, int32_t b, uint8_t* out) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!out || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    st = ensure_params(c, 1);
+    if (st != TWG_OK) return st;
+    ScenParams sp;
+    std::memset(&sp, 0, sizeof(sp));
+    sp.b = b;
+    sp.cur = c->cur[b];
+    void* hp = nullptr;
+    TWG_CUDA(c, stage_alloc(c, sizeof(ScenParams), &hp));
+    std::memcpy(hp, &sp, sizeof(sp));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_params, hp, sizeof(ScenParams), cudaMemcpyHostToDevice, c->stream));
+    PathArgs p;
+    std::memset(&p, 0, sizeof(p));
+    p.u0 = c->u[0];
+    p.u1 = c->u[1];
+    p.P = c->P;
+    p.sstride = c->sstride;
+    p.W = c->W;
+    p.H = c->H;
+    p.params = c->d_params;
+    p.nscen = 1;
+    p.dir = c->d_dir;
+    p.istride = c->sstride;
+    TWG_CUDA(c, launch_index_dir(p, c->stream));
+    c->launches += 1;
+    // [H][P] -> [H][W] (cudaMemcpyDefault: out may be host or device)
+    TWG_CUDA(c, cudaMemcpy2DAsync(out, c->W, c->d_dir + (int64_t)b * c->sstride, c->P, c->W, c->H, cudaMemcpyDefault,
+                                  c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_warp_map(twg_ctx* c, const twg_robot* robot, double warp_spacing, int32_t* out) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!out || !robot || !(warp_spacing > 0.0)) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    const double cth = std::cos(robot->theta), sth = std::sin(robot->theta);  // host libm (C25)
+    const size_t bytes = (size_t)c->W * c->H * sizeof(int32_t);
+    int32_t* dst = out;
+    if (!is_device_ptr(out)) TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&dst), bytes, c->stream));
+    TWG_CUDA(c, launch_warp_map(dst, c->W, c->H, c->cs, c->ox, c->oy, robot->x, robot->y, cth, sth, warp_spacing,
+                                c->stream));
+    c->launches += 1;
+    if (dst != out) {
+        TWG_CUDA(c, cudaMemcpyAsync(out, dst, bytes, cudaMemcpyDeviceToHost, c->stream));
+        TWG_CUDA(c, cudaFreeAsync(dst, c->stream));
+    }
     TWG_CUDA(c, cudaStreamSynchronize(c->stream));
     return TWG_OK;
 }

@@ -206,6 +206,70 @@ __global__ void k_rb_simple(float* __restrict__ u, int64_t P, int64_t sstride, i
     }
 }
 
+// ---------------------------------------------------------------- Jacobi
+// Eq. 1: every free cell from the previous iterate, u <- 0.25 ((E + W) + (N + S)), read
+// from buffer cur[b] ^ lp and written to the other one (fixed cells copied through).  One sweep per
+// launch; HBM-bound (4 B read + 4 B written per cell).  A warp owns a 128-column strip (float4 per
+// lane) and marches down kJacRows rows keeping rows y - 1, y, y + 1 in registers; the E/W neighbours
+// come from the adjacent lanes by shuffle, the strip-edge ones from two scalar loads.
+constexpr int kJacRows = 16, kJacWarps = 4;
+
+__device__ __forceinline__ float jac_cell(float c, float e, float w, float n, float s, float& dmax, bool count) {
+    if (!is_free(c)) return c;
+    const float nv = 0.25f * ((fabsf(e) + fabsf(w)) + (fabsf(n) + fabsf(s)));
+    if (count) dmax = fmaxf(dmax, fabsf(-nv - c));
+    return -nv;
+}
+
+__global__ void __launch_bounds__(kJacWarps * 32) k_jacobi(RelaxArgs a, int resid) {
+    const int b = blockIdx.z;
+    if (a.done[b]) return;
+    const int lane = threadIdx.x & 31;
+    const int x0 = blockIdx.x * kStripW;
+    const int x = x0 + 4 * lane;
+    const int y0 = (blockIdx.y * kJacWarps + (threadIdx.x >> 5)) * kJacRows;
+    if (y0 >= a.H) return;  // warp-uniform
+    const int src_i = a.cur[b] ^ a.lp;
+    const float* __restrict__ src = (src_i ? a.u1 : a.u0) + (int64_t)b * a.sstride;
+    float* __restrict__ dst = (src_i ? a.u0 : a.u1) + (int64_t)b * a.sstride;
+    const bool in = x < a.P;  // P is a multiple of 32: a float4 is wholly inside or outside the row
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto ld4 = [&](int y) -> float4 {
+        return (in && y >= 0 && y < a.H) ? __ldg(reinterpret_cast<const float4*>(src + (int64_t)y * a.P + x)) : zero;
+    };
+    float4 up = ld4(y0 - 1), c = ld4(y0);
+    const int y1 = min(y0 + kJacRows, a.H);
+    float dmax = 0.0f;
+    for (int y = y0; y < y1; ++y) {
+        const float4 dn = ld4(y + 1);
+        float wv = __shfl_up_sync(0xffffffffu, c.w, 1);
+        float ev = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (lane == 0) wv = x0 > 0 ? __ldg(src + (int64_t)y * a.P + x0 - 1) : 0.0f;
+        if (lane == 31) ev = x0 + kStripW < a.P ? __ldg(src + (int64_t)y * a.P + x0 + kStripW) : 0.0f;
+        if (in) {
+            const bool count = resid && y >= a.res_r0 && y < a.res_r1;
+            float4 o;
+            o.x = jac_cell(c.x, c.y, wv, up.x, dn.x, dmax, count);
+            o.y = jac_cell(c.y, c.z, c.x, up.y, dn.y, dmax, count);
+            o.z = jac_cell(c.z, c.w, c.y, up.z, dn.z, dmax, count);
+            o.w = jac_cell(c.w, ev, c.z, up.w, dn.w, dmax, count);
+            *reinterpret_cast<float4*>(dst + (int64_t)y * a.P + x) = o;
+        }
+        up = c;
+        c = dn;
+    }
+    if (resid) {
+        const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(dmax));
+        if (lane == 0 && m != 0u) atomicMax(&a.res[b], m);
+    }
+}
+
+cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st) {
+    dim3 grid((unsigned)((a.P + kStripW - 1) / kStripW), (a.H + kJacWarps * kJacRows - 1) / (kJacWarps * kJacRows), B);
+    k_jacobi<<<grid, kJacWarps * 32, 0, st>>>(a, resid ? 1 : 0);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- convergence control (a6)
 // After a chunk of `chunk` sweeps whose last launch accumulated the residual:
 // sweeps += chunk; stop when (sweeps % check_every == 0 && res < tol) or
@@ -292,6 +356,7 @@ void preload_relax_kernels() {
     preload_T<5>(); preload_T<6>(); preload_T<7>(); preload_T<8>();
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, k_rb_simple);
+    cudaFuncGetAttributes(&a, k_jacobi);
     cudaFuncGetAttributes(&a, k_check);
     cudaFuncGetAttributes(&a, k_fixup);
     cudaGetLastError();

@@ -82,11 +82,20 @@ __global__ void k_track_predict(EncodeArgs e) {
     double tf = ceil(rx / w.w);
     if (tf < 1.0) tf = 1.0;
     const int t = (int)tf;
-    // a2: horizon j = clamp(round(v t), 0, hmax), v = speed_r / max(|v_hat|, eps_v) (Eq. 16, C18)
-    double so = sqrt(tr.x[2] * tr.x[2] + tr.x[3] * tr.x[3]);
-    if (so < w.eps_v) so = w.eps_v;
-    const double v = sp.speed / so;
-    long long jl = round_half_away(v * (double)t);
+    long long jl;
+    if (w.hmode == 0) {
+        // a2: horizon j = clamp(round(v t), 0, hmax), v = speed_r / max(|v_hat|, eps_v) (Eq. 16, C18)
+        double so = sqrt(tr.x[2] * tr.x[2] + tr.x[3] * tr.x[3]);
+        if (so < w.eps_v) so = w.eps_v;
+        const double v = sp.speed / so;
+        jl = round_half_away(v * (double)t);
+    } else if (!(sp.speed > 0.0)) {
+        jl = w.hmax;  // robot at rest never reaches the ring (C26)
+    } else {
+        // ring time: j = round(t w / (speed_r dt)) (C26)
+        const double steps = ((double)t * w.w) / (sp.speed * w.dt);
+        jl = steps < 0.0 ? -round_half_away(-steps) : round_half_away(steps);
+    }
     if (jl < 0) jl = 0;
     if (jl > w.hmax) jl = w.hmax;
     const int j = (int)jl;
@@ -130,8 +139,9 @@ __global__ void k_track_predict(EncodeArgs e) {
                 Pc[r * 4 + col] = acc + w.Q[r * 4 + col];
             }
     }
-    // footprint: sigma^2 = (P00 + P11) / 2; Gaussian >= 1/2 <=> d^2 <= 2 ln2 sigma^2; U safety disk (C20)
-    const double sig2 = (Pc[0] + Pc[5]) * 0.5;
+    // footprint: sigma^2 = (P00 + P11) / 2 of the predicted (C19) or posterior (C27) covariance;
+    // Gaussian >= 1/2 <=> d^2 <= 2 ln2 sigma^2; U safety disk (C20)
+    const double sig2 = w.fmode == 0 ? (Pc[0] + Pc[5]) * 0.5 : (tr.P[0] + tr.P[5]) * 0.5;
     const double g = 1.3862943611198906 * sig2;
     const double s2 = w.rs * w.rs;
     const double R2 = g > s2 ? g : s2;
@@ -249,8 +259,12 @@ cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nsce
     return cudaGetLastError();
 }
 
+__global__ void k_warp_map(int32_t* __restrict__ out, int W, int H, double cs, double ox, double oy, double xr,
+                           double yr, double c, double s, double w);
+
 void preload_stamp_kernels() {
     cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, k_warp_map);
     cudaFuncGetAttributes(&a, k_encode_cold);
     cudaFuncGetAttributes(&a, k_unstamp);
     cudaFuncGetAttributes(&a, k_goal_reset);
@@ -287,6 +301,32 @@ cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_track
     k_set_goal<<<sb, 128, 0, st>>>(e);
     ++nl;
     if (n_launch) *n_launch = nl;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ per-cell warp map (f3)
+// The paper's kernel 1 ("calculate the warp of each cell"): t = max(1, ceil(r_x / w)) of an
+// obstacle at each cell centre, r_x the Eq. 15 closed form (C16) -- the same fp64 sequence as
+// k_track_predict.  out: [H][W] int32.
+__global__ void k_warp_map(int32_t* __restrict__ out, int W, int H, double cs, double ox, double oy, double xr,
+                           double yr, double c, double s, double w) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= W) return;
+    const double px = ox + ((double)x + 0.5) * cs;
+    const double py = oy + ((double)y + 0.5) * cs;
+    const double dx = px - xr, dy = py - yr;
+    const double aa = c * dx + s * dy;
+    const double bb = s * dx - c * dy;
+    const double rx = (sqrt(4.0 * aa * aa + 12.16 * bb * bb) - 1.8 * aa) / 0.38;
+    double tf = ceil(rx / w);
+    if (tf < 1.0) tf = 1.0;
+    out[(int64_t)y * W + x] = (int32_t)tf;
+}
+
+cudaError_t launch_warp_map(int32_t* out, int W, int H, double cs, double ox, double oy, double xr, double yr, double c,
+                            double s, double w, cudaStream_t st) {
+    k_warp_map<<<dim3((W + 255) / 256, H), 256, 0, st>>>(out, W, H, cs, ox, oy, xr, yr, c, s, w);
     return cudaGetLastError();
 }
 

@@ -59,6 +59,8 @@ struct ScenParams {
 struct WarpCfgDev {
     double dt, Q[16], w, eps_v, rs;
     int hmax;
+    int hmode;  // 0: Eq. 16 (C18); 1: ring time (C26)
+    int fmode;  // 0: predicted covariance (C19); 1: posterior covariance (C27)
 };
 
 struct PathMeta {  // per scenario, written by k_walk / k_band

@@ -7,6 +7,9 @@ namespace twg {
 // k_relax.cu (rows a4-a6)
 cudaError_t launch_rb_tblock(int T, const CUtensorMap& map0, const CUtensorMap& map1, const RelaxArgs& a, int B, int qoff, bool resid,
                              cudaStream_t st);
+cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st);
+cudaError_t launch_warp_map(int32_t* out, int W, int H, double cs, double ox, double oy, double xr, double yr, double c,
+                            double s, double w, cudaStream_t st);
 cudaError_t launch_rb_simple(float* u, int64_t P, int64_t sstride, int W, int H, int B, int color, int row_off,
                              const int* done, unsigned* res, cudaStream_t st);
 cudaError_t launch_check(int B, int* done, int* sweeps, unsigned* res_bits, float* res_final, int* where, int chunk,
@@ -63,6 +66,7 @@ struct PathArgs {
     CUtensorMap idx_map;   // M_idx as a 2D {P, H * B} uint16 tensor, box {256, 176}
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
+cudaError_t launch_index_dir(const PathArgs& p, cudaStream_t st);  // k_index_dir alone (twg_index_matrix)
 
 // Module preloading (called once by twg_create)
 void preload_relax_kernels();

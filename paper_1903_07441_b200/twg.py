@@ -37,13 +37,14 @@ class Track(C.Structure):
 
 class WarpCfg(C.Structure):
     _fields_ = [("dt", C.c_double), ("Q", C.c_double * 16), ("warp_spacing", C.c_double), ("eps_v", C.c_double),
-                ("safety_radius", C.c_double), ("horizon_max", C.c_int32), ("reserved", C.c_int32)]
+                ("safety_radius", C.c_double), ("horizon_max", C.c_int32), ("horizon_mode", C.c_int32),
+                ("footprint_mode", C.c_int32), ("reserved", C.c_int32)]
 
 
 class RelaxCfg(C.Structure):
     _fields_ = [("max_sweeps", C.c_int32), ("check_every", C.c_int32), ("warm_start", C.c_int32),
                 ("temporal_depth", C.c_int32), ("tol", C.c_float), ("rows_per_warp", C.c_int32),
-                ("sync_every", C.c_int32), ("reserved", C.c_int32)]
+                ("sync_every", C.c_int32), ("mode", C.c_int32)]
 
 
 class BandCfg(C.Structure):
@@ -71,6 +72,8 @@ SIGNATURES = [
     ("twg_get_field", C.c_int32, [_P, C.c_int32, _P, C.c_int32]),
     ("twg_set_field", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_get_warp", C.c_int32, [_P, C.c_int32, C.c_int32, _P, _P, _P]),
+    ("twg_index_matrix", C.c_int32, [_P, C.c_int32, _P]),
+    ("twg_warp_map", C.c_int32, [_P, C.POINTER(Robot), C.c_double, _P]),
     ("twg_field_ptr", C.c_int32, [_P, C.c_int32, C.POINTER(_P), C.POINTER(C.c_int64)]),
     ("twg_debug_walk", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_kernel_launches", C.c_int64, [_P]),
@@ -122,7 +125,8 @@ def _check(ctx, st, ok=(OK, W_GOAL_SWALLOWED, W_TRUNCATED)):
     return st
 
 
-def warp_cfg(dt=0.1, Q=None, warp_spacing=1.0, eps_v=0.05, safety_radius=0.5, horizon_max=20):
+def warp_cfg(dt=0.1, Q=None, warp_spacing=1.0, eps_v=0.05, safety_radius=0.5, horizon_max=20, horizon_mode=0,
+             footprint_mode=0):
     c = WarpCfg()
     c.dt = dt
     q = np.zeros(16) if Q is None else np.asarray(Q, np.float64).reshape(16)
@@ -132,12 +136,14 @@ def warp_cfg(dt=0.1, Q=None, warp_spacing=1.0, eps_v=0.05, safety_radius=0.5, ho
     for k in range(16):
         c.Q[k] = float(q[k])
     c.warp_spacing, c.eps_v, c.safety_radius, c.horizon_max = warp_spacing, eps_v, safety_radius, horizon_max
+    c.horizon_mode, c.footprint_mode = horizon_mode, footprint_mode
     return c
 
 
 def relax_cfg(max_sweeps=100, check_every=0, warm_start=1, temporal_depth=0, tol=0.0, rows_per_warp=0,
-              sync_every=0):
-    return RelaxCfg(max_sweeps, check_every, warm_start, temporal_depth, tol, rows_per_warp, sync_every, 0)
+              sync_every=0, mode=0):
+    """mode 0: red-black Gauss-Seidel (Eq. 2); 1: Jacobi (Eq. 1)."""
+    return RelaxCfg(max_sweeps, check_every, warm_start, temporal_depth, tol, rows_per_warp, sync_every, mode)
 
 
 def band_cfg(iterations=50, max_len=4096, max_smooth=8192, step=0.25, k_t=1.0):
@@ -240,6 +246,19 @@ class Planner:
         pred = np.zeros((max(n, 1), 3))
         _check(self.ctx, lib().twg_get_warp(self.ctx, b, n, _ptr(t), _ptr(j), _ptr(pred)))
         return t[:n], j[:n], pred[:n]
+
+    def index_matrix(self, b=0, out=None):
+        """twg_index_matrix: uint8 [H, W] M_idx of scenario b (0..3 move, 4 goal, 5 obstacle, 6 none)."""
+        out = np.zeros((self.H, self.W), np.uint8) if out is None else out
+        _check(self.ctx, lib().twg_index_matrix(self.ctx, b, _ptr(out)))
+        return out
+
+    def warp_map(self, robot, warp_spacing=1.0, out=None):
+        """twg_warp_map: int32 [H, W] warp number of every cell centre for the robot pose."""
+        out = np.zeros((self.H, self.W), np.int32) if out is None else out
+        r = Robot(*[float(v) for v in robot])
+        _check(self.ctx, lib().twg_warp_map(self.ctx, C.byref(r), float(warp_spacing), _ptr(out)))
+        return out
 
     def field_ptr(self, b=0):
         p = C.c_void_p()
