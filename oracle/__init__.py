@@ -73,6 +73,12 @@ def lib():
         L.orc_relax_jacobi_f32.argtypes = [i32, i32, P, P, i32, i32, f32, P]
         L.orc_index_matrix.restype = None
         L.orc_index_matrix.argtypes = [i32, i32, P, P, P]
+        L.orc_kalman_update.restype = i32
+        L.orc_kalman_update.argtypes = [P, P, P, P]
+        L.orc_associate.restype = None
+        L.orc_associate.argtypes = [i32, P, i32, P, d, P, P]
+        L.orc_track_step.restype = i32
+        L.orc_track_step.argtypes = [i32, P, P, i32, i32, P, d, P, d, d, d, d, i32, i32, P]
         L.orc_warp_map.restype = None
         L.orc_warp_map.argtypes = [i32, i32, d, d, d, d, d, d, d, P]
         L.orc_init_u32.restype = None
@@ -253,6 +259,52 @@ def warp_map(scene):
     lib().orc_warp_map(scene.W, scene.H, scene.cell_size, scene.origin[0], scene.origin[1], xr, yr, th,
                        scene.warp.warp_spacing, _p(out))
     return out
+
+
+W_TRUNCATED, W_SINGULAR = 2, 3
+
+
+def kalman_update(x, P, z, R):
+    """Eqs. 11-13 (returns status, x', P'); inputs are not modified."""
+    x = np.array(x, np.float64).reshape(4).copy()
+    P = np.array(P, np.float64).reshape(16).copy()
+    z = np.ascontiguousarray(z, np.float64).reshape(2)
+    R = np.ascontiguousarray(R, np.float64).reshape(4)
+    st = lib().orc_kalman_update(_p(x), _p(P), _p(z), _p(R))
+    return st, x, P.reshape(4, 4)
+
+
+def associate(pxy, z, gate):
+    pxy = np.ascontiguousarray(pxy, np.float64).reshape(-1, 2)
+    z = np.ascontiguousarray(z, np.float64).reshape(-1, 2)
+    n, m = len(pxy), len(z)
+    mt = np.zeros(max(n, 1), np.int32)
+    du = np.zeros(max(m, 1), np.uint8)
+    lib().orc_associate(n, _p(pxy), m, _p(z), float(gate), _p(mt), _p(du))
+    return mt[:n], du[:m].astype(bool)
+
+
+def track_step(tracks, missed, z, dt=0.1, Q=None, sigma_z=0.05, gate=0.5, var_pos=0.25, var_vel=1.0,
+               prune_after=10, max_tracks=0):
+    """One tracker tick (orc_track_step).  tracks [n, 20], missed [n], z [m, 2] -> (status, tracks, missed)."""
+    tracks = np.asarray(tracks, np.float64).reshape(-1, 20)
+    z = np.ascontiguousarray(z, np.float64).reshape(-1, 2)
+    n, m = len(tracks), len(z)
+    cap = n + m + 1
+    trk = np.zeros((cap, 20))
+    trk[:n] = tracks
+    mis = np.zeros(cap, np.int32)
+    mis[:n] = np.asarray(missed, np.int32).reshape(n)
+    if Q is None:
+        Q = np.zeros(16)
+        Q[0] = Q[5] = 1e-3 * dt ** 4 / 4.0
+        Q[10] = Q[15] = 1e-3 * dt ** 2
+    Q = np.ascontiguousarray(Q, np.float64).reshape(16)
+    n_out = np.zeros(1, np.int32)
+    st = lib().orc_track_step(n, _p(trk), _p(mis), cap, m, _p(z), float(dt), _p(Q), float(sigma_z), float(gate),
+                              float(var_pos), float(var_vel), int(prune_after), int(max_tracks), _p(n_out))
+    k = int(n_out[0])
+    return st, trk[:k].copy(), mis[:k].copy()
 
 
 def jacobi_f64(cls, u, max_sweeps, tol=0.0):

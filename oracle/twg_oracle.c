@@ -644,3 +644,175 @@ int32_t orc_next_waypoint(int32_t n, const float* pts, float* nx, float* ny)
     *nx = pts[2 * (n - 1)]; *ny = pts[2 * (n - 1) + 1];
     return n - 1;
 }
+
+/* ------------------------------------------------------------------------ */
+/* f1  Kalman update, association, spawn/prune (the step before a1)         */
+/* (Eqs. 11-13; H of P:558-565; R = sigma_z^2 I, P:569-572 and    */
+/* S:307; association and track management S:281-298, C28-C30)             */
+/* ------------------------------------------------------------------------ */
+
+enum { ORC_W_TRUNCATED = 2, ORC_W_SINGULAR = 3 };
+
+/* Eqs. 11-13 written out with the explicit H = [I2 0]:
+ *   K = P H^T (H P H^T + R)^-1;  x <- x + K (z - H x);  P <- (I - K H) P,
+ * then P <- (P + P^T) / 2 (C28).  The 2x2 inverse is the adjugate over the
+ * determinant.  Returns 0, or -1 (x, P untouched) when H P H^T + R is not
+ * positive definite (S:276 SingularInnovation). */
+int32_t orc_kalman_update(double* x, double* P, const double* z, const double* R)
+{
+    static const double Hm[8] = { 1.0, 0.0, 0.0, 0.0,
+                                  0.0, 1.0, 0.0, 0.0 };
+    double Hx[2], y[2], HP[8], S[4], Si[4], PHt[8], K[8], IKH[16], Pn[16], xn[4];
+    for (int r = 0; r < 2; ++r) {
+        double acc = 0.0;
+        for (int k = 0; k < 4; ++k) acc = acc + Hm[r * 4 + k] * x[k];
+        Hx[r] = acc;
+        y[r] = z[r] - Hx[r];
+    }
+    for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 4; ++c) {
+            double acc = 0.0;
+            for (int k = 0; k < 4; ++k) acc = acc + Hm[r * 4 + k] * P[k * 4 + c];
+            HP[r * 4 + c] = acc;
+        }
+    for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 2; ++c) {
+            double acc = 0.0;
+            for (int k = 0; k < 4; ++k) acc = acc + HP[r * 4 + k] * Hm[c * 4 + k];
+            S[r * 2 + c] = acc + R[r * 2 + c];
+        }
+    double det = S[0] * S[3] - S[1] * S[2];
+    if (!(det > 0.0) || !(S[0] > 0.0) || !(det < 1.0e300)) return -1;
+    Si[0] = S[3] / det;
+    Si[1] = -S[1] / det;
+    Si[2] = -S[2] / det;
+    Si[3] = S[0] / det;
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 2; ++c) {
+            double acc = 0.0;
+            for (int k = 0; k < 4; ++k) acc = acc + P[r * 4 + k] * Hm[c * 4 + k];
+            PHt[r * 2 + c] = acc;
+        }
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 2; ++c) {
+            double acc = 0.0;
+            for (int k = 0; k < 2; ++k) acc = acc + PHt[r * 2 + k] * Si[k * 2 + c];
+            K[r * 2 + c] = acc;
+        }
+    for (int r = 0; r < 4; ++r) {
+        double acc = 0.0;
+        for (int k = 0; k < 2; ++k) acc = acc + K[r * 2 + k] * y[k];
+        xn[r] = x[r] + acc;
+    }
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+            double acc = 0.0;
+            for (int k = 0; k < 2; ++k) acc = acc + K[r * 2 + k] * Hm[k * 4 + c];
+            IKH[r * 4 + c] = (r == c ? 1.0 : 0.0) - acc;
+        }
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+            double acc = 0.0;
+            for (int k = 0; k < 4; ++k) acc = acc + IKH[r * 4 + k] * P[k * 4 + c];
+            Pn[r * 4 + c] = acc;
+        }
+    for (int r = 0; r < 4; ++r) x[r] = xn[r];
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) P[r * 4 + c] = 0.5 * (Pn[r * 4 + c] + Pn[c * 4 + r]);
+    return 0;
+}
+
+/* Greedy gated nearest neighbour (the paper is silent, C29):
+ * repeatedly take the globally closest still-free (track, detection) pair
+ * with squared distance dx*dx + dy*dy <= gate^2 (dx = z_x - x_pred), ties to
+ * the lower track index, then the lower detection index.  pxy[2 n] predicted
+ * positions, z[2 m] detections; match_t[n] = detection or -1; det_used[m]. */
+void orc_associate(int32_t n, const double* pxy, int32_t m, const double* z, double gate,
+                   int32_t* match_t, uint8_t* det_used)
+{
+    double g2 = gate * gate;
+    for (int32_t i = 0; i < n; ++i) match_t[i] = -1;
+    for (int32_t j = 0; j < m; ++j) det_used[j] = 0;
+    for (;;) {
+        int32_t bi = -1, bj = -1;
+        double bd = 0.0;
+        for (int32_t i = 0; i < n; ++i) {
+            if (match_t[i] >= 0) continue;
+            for (int32_t j = 0; j < m; ++j) {
+                if (det_used[j]) continue;
+                double dx = z[2 * j] - pxy[2 * i];
+                double dy = z[2 * j + 1] - pxy[2 * i + 1];
+                double d2 = dx * dx + dy * dy;
+                if (d2 <= g2 && (bi < 0 || d2 < bd)) { bd = d2; bi = i; bj = j; }
+            }
+        }
+        if (bi < 0) break;
+        match_t[bi] = bj;
+        det_used[bj] = 1;
+    }
+}
+
+/* One tracker tick (Alg. 1 P:680-688 "Read ... Detect ... Estimate", C30):
+ *   1. predict every track one step (Eqs. 9-10, orc_predict with j = 1);
+ *   2. associate detections with the predicted positions (orc_associate);
+ *   3. matched: Eqs. 11-13 with R = sigma_z^2 I, missed = 0 (singular
+ *      innovation: keeps the prediction, missed + 1, warning);
+ *      unmatched: keeps the prediction, missed + 1;
+ *   4. prune tracks with missed > prune_after, keeping the order;
+ *   5. append one track per unmatched detection in detection order:
+ *      x = (z, 0, 0), P = diag(var_pos, var_pos, var_vel, var_vel);
+ *   6. keep at most max_tracks (> 0) tracks, survivors first (warning).
+ * trk[cap][20] (x[4], P[16]) and missed[cap] in/out, cap >= n + m.
+ * Returns ORC_OK, ORC_W_TRUNCATED or ORC_W_SINGULAR (the larger code wins). */
+int32_t orc_track_step(int32_t n, double* trk, int32_t* missed, int32_t cap, int32_t m, const double* z,
+                       double dt, const double* Q, double sigma_z, double gate, double var_pos,
+                       double var_vel, int32_t prune_after, int32_t max_tracks, int32_t* n_out)
+{
+    int32_t status = ORC_OK;
+    double* pred = (double*)malloc(sizeof(double) * 20 * (size_t)(n > 0 ? n : 1));
+    double* pxy = (double*)calloc(2 * (size_t)(n > 0 ? n : 1), sizeof(double));
+    int32_t* mt = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    int32_t* mis = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    uint8_t* du = (uint8_t*)malloc((size_t)(m > 0 ? m : 1));
+    double R[4] = { sigma_z * sigma_z, 0.0, 0.0, sigma_z * sigma_z };
+    for (int32_t i = 0; i < n; ++i) {
+        orc_predict(trk + 20 * i, trk + 20 * i + 4, Q, dt, 1, pred + 20 * i, pred + 20 * i + 4);
+        pxy[2 * i] = pred[20 * i];
+        pxy[2 * i + 1] = pred[20 * i + 1];
+    }
+    orc_associate(n, pxy, m, z, gate, mt, du);
+    for (int32_t i = 0; i < n; ++i) {
+        mis[i] = missed[i] + 1;
+        if (mt[i] >= 0) {
+            if (orc_kalman_update(pred + 20 * i, pred + 20 * i + 4, z + 2 * mt[i], R) == 0) mis[i] = 0;
+            else status = ORC_W_SINGULAR;
+        }
+    }
+    int32_t limit = max_tracks > 0 ? max_tracks : cap;
+    if (limit > cap) limit = cap;
+    int32_t k = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (mis[i] > prune_after) continue;
+        if (k >= limit) { if (status < ORC_W_TRUNCATED) status = ORC_W_TRUNCATED; continue; }
+        memcpy(trk + 20 * k, pred + 20 * i, 20 * sizeof(double));
+        missed[k] = mis[i];
+        ++k;
+    }
+    for (int32_t j = 0; j < m; ++j) {
+        if (du[j]) continue;
+        if (k >= limit) { if (status < ORC_W_TRUNCATED) status = ORC_W_TRUNCATED; continue; }
+        double* t = trk + 20 * k;
+        memset(t, 0, 20 * sizeof(double));
+        t[0] = z[2 * j];
+        t[1] = z[2 * j + 1];
+        t[4 + 0] = var_pos;
+        t[4 + 5] = var_pos;
+        t[4 + 10] = var_vel;
+        t[4 + 15] = var_vel;
+        missed[k] = 0;
+        ++k;
+    }
+    *n_out = k;
+    free(pred); free(pxy); free(mt); free(mis); free(du);
+    return status;
+}

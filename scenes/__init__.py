@@ -18,6 +18,7 @@ from .gen import (  # noqa: F401
     scene_c4,
     scene_c5,
     advance_scene,
+    detections,
     annulus_fixed,
     random_small_map,
     CONFIGS,

@@ -219,6 +219,23 @@ def advance_scene(scene: Scene, tick: int, robot_step: float = 0.04) -> Scene:
     return replace(scene, name=f"{scene.name}_t{tick}", robot=(rx2, ry2, th, sp), tracks=tracks, truth=truth)
 
 
+def detections(scene: Scene, tick: int, sigma_z: float = 0.05, p_miss: float = 0.05, n_clutter: int = 0,
+               shuffle: bool = True) -> np.ndarray:
+    """Noisy position detections [m, 2] of the obstacle truths at tick `tick` (advance_scene motion):
+    each truth is seen with probability 1 - p_miss, with N(0, sigma_z^2) noise per axis,
+    plus `n_clutter` uniform false detections, in random order.  Input plumbing only."""
+    rng = np.random.default_rng([scene.seed, tick, 7])
+    truth = advance_scene(scene, tick).truth if tick else scene.truth
+    seen = rng.random(len(truth)) >= p_miss
+    z = truth[seen, :2] + rng.normal(0.0, sigma_z, (int(seen.sum()), 2))
+    if n_clutter:
+        ext = np.array([scene.W * scene.cell_size, scene.H * scene.cell_size])
+        z = np.concatenate([z, rng.uniform(0.0, 1.0, (n_clutter, 2)) * ext])
+    if shuffle:
+        z = z[rng.permutation(len(z))]
+    return np.ascontiguousarray(z)
+
+
 def random_small_map(seed: int, N: int = 48, n_disks=(3, 11), n_walls=(0, 4)):
     """Random N x N static map with disks and walls plus a goal cell and a start cell.
 
