@@ -58,7 +58,9 @@ typedef int32_t twg_status;
 enum {
     TWG_OK = 0,
     TWG_W_GOAL_SWALLOWED = 1,      /* a footprint covered the goal cell; the goal was kept */
-    TWG_W_TRUNCATED = 2,           /* smoothed path longer than max_smooth; output truncated */
+    TWG_W_TRUNCATED = 2,           /* output longer than its capacity; truncated */
+    TWG_W_SINGULAR_INNOVATION = 3, /* a matched track's H P H^T + R was not positive definite;
+                                      the track kept its prediction */
     TWG_E_INVALID_ARG = -1,
     TWG_E_OUT_OF_BOUNDS = -2,      /* goal or robot cell outside the grid */
     TWG_E_OVERLAPPING_CLASSES = -3,/* goal on a static wall */
@@ -149,6 +151,23 @@ typedef struct {
     float step, k_t;
 } twg_band_cfg;
 
+/* Tracker configuration (row f1, the step before a1 in Alg. 1's Map Update,
+ * P:680-688):
+ *   sigma_z [0.05 m]: measurement noise, R = sigma_z^2 I;
+ *   gate [0.5 m]: a (track, detection) pair is a candidate iff the squared
+ *     distance from the predicted position is <= gate^2;
+ *   spawn_var_pos [0.25 m^2], spawn_var_vel [1.0 (m/s)^2]: covariance
+ *     diagonal of a track spawned from an unmatched detection;
+ *   prune_after [10]: tracks with missed > prune_after are removed;
+ *   max_tracks [0 = no limit]: tracks kept per scenario after the tick. */
+typedef struct {
+    double sigma_z, gate, spawn_var_pos, spawn_var_vel;
+    int32_t prune_after, max_tracks;
+} twg_tracker_cfg;
+
+/* n / n_tracks value selecting the context's resident tracker table. */
+#define TWG_RESIDENT_TRACKS (-1)
+
 /* Result of one planning tick.  next_x/next_y: next waypoint in cell units
  * (cell (i, k) has centre (i + 0.5, k + 0.5)) (Alg. 1). */
 typedef struct {
@@ -189,7 +208,10 @@ TWG_API twg_status twg_set_static(twg_ctx* ctx, int32_t b, const uint8_t* occ);
  * warm = 1: every free cell keeps the value it holds, including cells fixed
  * in the previous call and free now (a released obstacle keeps u = 0, a
  * released goal u = 1) ("the values evolve slowly"; C7).
- * tracks: n entries, host or device pointer (n may be 0).
+ * tracks: n entries, host or device pointer (n may be 0); they also replace
+ * the scenario's resident tracker table (missed counters 0).  tracks = NULL
+ * with n = TWG_RESIDENT_TRACKS: use the resident table as left by
+ * twg_track_update (row f1).
  * Returns OK, W_GOAL_SWALLOWED, or OUT_OF_BOUNDS / OVERLAPPING_CLASSES /
  * INVALID_START / INVALID_ARG (validated before any device work). */
 TWG_API twg_status twg_set_obstacles(twg_ctx* ctx, int32_t b, const twg_robot* robot,
@@ -226,7 +248,9 @@ TWG_API twg_status twg_extract_path(twg_ctx* ctx, int32_t b, const twg_band_cfg*
  *   concatenation of n_tracks[0..batch) tracks, out[batch],
  *   cells_xy[batch][2 max_len], smooth_xy[batch][2 max_smooth].
  * tracks may be host or device; every other pointer is host (cells_xy,
- * smooth_xy may be NULL).  Returns the worst per-scenario status. */
+ * smooth_xy may be NULL).  tracks = NULL and n_tracks = NULL: every
+ * scenario uses its resident tracker table (row f1).
+ * Returns the worst per-scenario status. */
 TWG_API twg_status twg_plan_step(twg_ctx* ctx, int32_t b, const twg_robot* robot, const int32_t* goal_xy,
                                  const twg_track* tracks, const int32_t* n_tracks,
                                  const twg_warp_cfg* warp, const twg_relax_cfg* relax,
@@ -246,6 +270,33 @@ TWG_API twg_status twg_set_field(twg_ctx* ctx, int32_t b, const float* raw);
  * for parity tests): t[n] warp numbers, j[n] horizons, pred[3 n] =
  * (x_pred, y_pred, R^2).  n must equal the track count of that call. */
 TWG_API twg_status twg_get_warp(twg_ctx* ctx, int32_t b, int32_t n, int32_t* t, int32_t* j, double* pred);
+
+/* Row f1: one tracker tick on the resident track table of scenario b
+ * (b = -1: every scenario) -- Alg. 1 P:680-688 "Read ... Detect ...
+ * Estimate":
+ *   1. every track predicted one step (Eqs. 9-10; dt, Q of `warp`);
+ *   2. greedy gated association: repeatedly the globally closest free
+ *      (track, detection) pair within the gate, ties to the lower track
+ *      then the lower detection index (C29);
+ *   3. matched tracks: Kalman update Eqs. 11-13 with
+ *      H = [I2 0], R = sigma_z^2 I, then P <- (P + P^T) / 2
+ *      (C28), missed = 0; unmatched tracks keep the prediction, missed + 1;
+ *   4. tracks with missed > prune_after removed, order kept;
+ *   5. one track per unmatched detection appended in detection order,
+ *      x = (z, 0, 0), P = diag(var_pos, var_pos, var_vel, var_vel);
+ *   6. at most max_tracks kept (survivors first; W_TRUNCATED).
+ * det_xy: (x, y) metres, host or device; b >= 0: n_det[0] detections;
+ * b = -1: the concatenation of n_det[0..batch) (host array) detections.
+ * n_tracks (host, may be NULL): track count per scenario after the tick.
+ * Synchronises.  Returns OK, W_TRUNCATED, W_SINGULAR_INNOVATION or
+ * INVALID_ARG (sigma_z, gate, variances < 0, prune_after < 0). */
+TWG_API twg_status twg_track_update(twg_ctx* ctx, int32_t b, const double* det_xy, const int32_t* n_det,
+                                    const twg_warp_cfg* warp, const twg_tracker_cfg* cfg, int32_t* n_tracks);
+
+/* Copy scenario b's resident tracker table: up to cap tracks into out and
+ * their missed counters into missed (host or device; either may be NULL);
+ * *n = the table's track count. */
+TWG_API twg_status twg_get_tracks(twg_ctx* ctx, int32_t b, twg_track* out, int32_t* missed, int32_t cap, int32_t* n);
 
 /* Full-grid index matrix M_idx of scenario b's current field (Eq. 3,
  * P:228-233; Alg. 1): out[height x width] uint8

@@ -11,6 +11,7 @@ from .twg import (  # noqa: F401
     warp_cfg,
     relax_cfg,
     band_cfg,
+    tracker_cfg,
     tracks_array,
     LIB_PATH,
 )

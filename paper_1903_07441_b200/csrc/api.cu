@@ -122,7 +122,9 @@ twg_status ensure_track_cap(twg_ctx* c, int cap) {
     int *t1, *t2;
     double* t3;
     int4* t4;
+    int* t5;
     TWG_CUDA(c, dev_alloc(&t0, B * nc));
+    TWG_CUDA(c, dev_alloc(&t5, B * nc));
     TWG_CUDA(c, dev_alloc(&t1, B * nc));
     TWG_CUDA(c, dev_alloc(&t2, B * nc));
     TWG_CUDA(c, dev_alloc(&t3, B * nc * 3));
@@ -139,18 +141,22 @@ twg_status ensure_track_cap(twg_ctx* c, int cap) {
                                       oc * 3 * sizeof(double), B, cudaMemcpyDeviceToDevice, c->stream));
         TWG_CUDA(c, cudaMemcpy2DAsync(t4, nc * sizeof(int4), c->d_boxes, oc * sizeof(int4), oc * sizeof(int4), B,
                                       cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaMemcpy2DAsync(t5, nc * sizeof(int), c->d_missed, oc * sizeof(int), oc * sizeof(int), B,
+                                      cudaMemcpyDeviceToDevice, c->stream));
         TWG_CUDA(c, cudaStreamSynchronize(c->stream));
         cudaFree(c->d_tracks);
         cudaFree(c->d_t);
         cudaFree(c->d_j);
         cudaFree(c->d_pred);
         cudaFree(c->d_boxes);
+        cudaFree(c->d_missed);
     }
     c->d_tracks = t0;
     c->d_t = t1;
     c->d_j = t2;
     c->d_pred = t3;
     c->d_boxes = t4;
+    c->d_missed = t5;
     c->track_cap = nc;
     return TWG_OK;
 }
@@ -221,8 +227,9 @@ twg_status validate(twg_ctx* c, const EncodeReq& r, int* rcx, int* rcy) {
 }
 
 // Rows a1-a3 for a list of scenarios.  tracks: concatenated per request (host or device).
+// resident: use the tracker tables (row f1) already in d_tracks instead of caller tracks.
 twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_track* tracks, const twg_warp_cfg* wc,
-                  int warm_req) {
+                  int warm_req, bool resident = false) {
     if (!wc) return fail(c, TWG_E_INVALID_ARG, "null warp cfg");
     if ((wc->horizon_mode != 0 && wc->horizon_mode != 1) || (wc->footprint_mode != 0 && wc->footprint_mode != 1))
         return fail(c, TWG_E_INVALID_ARG, "horizon_mode / footprint_mode must be 0 or 1");
@@ -265,7 +272,7 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     if (st != TWG_OK) return st;
     // tracks -> [B][cap]: one contiguous copy (device input: in place; host input: through the pinned
     // staging ring and one H2D copy) and one scatter kernel for every scenario of the call
-    if (total > 0) {
+    if (total > 0 && !resident) {
         const twg_track* src = tracks;
         if (!is_device_ptr(tracks)) {
             if (c->track_tmp_cap < total) {
@@ -299,8 +306,8 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
         std::memcpy(hs, off.data(), (ns + 1) * sizeof(int));
         std::memcpy(hs + ns + 1, sb.data(), ns * sizeof(int));
         TWG_CUDA(c, cudaMemcpyAsync(c->d_track_off, hs, (2 * ns + 1) * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        TWG_CUDA(c, launch_scatter_tracks(src, c->d_track_off, ns, c->d_track_off + ns + 1, c->d_tracks, c->track_cap,
-                                          c->stream));
+        TWG_CUDA(c, launch_scatter_tracks(src, c->d_track_off, ns, c->d_track_off + ns + 1, c->d_tracks, c->d_missed,
+                                          c->track_cap, c->stream));
         c->launches += 1;
     }
     // per-scenario params + cfg (pinned staging, one copy each)
@@ -356,6 +363,7 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
         sc.rcx = ps[k].rcx;
         sc.rcy = ps[k].rcy;
         sc.n_tracks = reqs[k].n;
+        if (!resident) sc.trk_n = reqs[k].n;
         sc.n_boxes = reqs[k].n;
         sc.encoded = true;
         sc.static_dirty = false;
@@ -638,6 +646,7 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
         preload_relax_kernels();
         preload_stamp_kernels();
         preload_path_kernels();
+        preload_track_kernels();
         preloaded = true;
     }
     CK(launch_init_field(c->u[0], c->P, c->sstride, c->W, c->H, c->B, c->stream));
@@ -663,7 +672,8 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
     void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_done,  c->d_sweeps, c->d_res_bits, c->d_res,
                     c->d_where,  c->d_cur,     c->d_flags, c->d_meta,  c->d_wcfg,   c->d_tracks,   c->d_t,
                     c->d_j,      c->d_pred,    c->d_boxes, c->d_params, c->d_track_off, c->d_cells, c->d_wp,
-                    c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir};
+                    c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
+                    c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -698,8 +708,10 @@ TWG_API twg_status twg_set_obstacles(twg_ctx* c, int32_t b, const twg_robot* rob
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!robot || b < 0 || b >= c->B || (n > 0 && !tracks)) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    const bool resident = !tracks && n == TWG_RESIDENT_TRACKS;
+    if (resident) n = c->scen[b].trk_n;
     EncodeReq r{b, *robot, goal_x, goal_y, n, 0};
-    st = encode(c, {r}, tracks, cfg, warm);
+    st = encode(c, {r}, tracks, cfg, warm, resident);
     if (st != TWG_OK) return st;
     int* hf = nullptr;
     TWG_CUDA(c, stage_alloc(c, sizeof(int), reinterpret_cast<void**>(&hf)));
@@ -753,21 +765,25 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
                                  int32_t* cells_xy, float* smooth_xy) {
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
-    if (!robot || !goal_xy || !n_tracks || !rcfg || !bcfg || !out || b < -1 || b >= c->B)
+    if (!robot || !goal_xy || !rcfg || !bcfg || !out || b < -1 || b >= c->B)
         return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    const bool resident = !tracks && !n_tracks;
+    if (!n_tracks && !resident) return fail(c, TWG_E_INVALID_ARG, "null n_tracks");
     if (c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "twg_plan_step is not available on a row slab");
     std::vector<EncodeReq> reqs;
     std::vector<int> bs;
     int64_t off = 0;
     const int ns = b < 0 ? c->B : 1;
     for (int k = 0; k < ns; ++k) {
-        EncodeReq r{b < 0 ? k : b, robot[k], goal_xy[2 * k], goal_xy[2 * k + 1], n_tracks[k], off};
-        off += n_tracks[k];
+        const int bk = b < 0 ? k : b;
+        const int nk = resident ? c->scen[bk].trk_n : n_tracks[k];
+        EncodeReq r{bk, robot[k], goal_xy[2 * k], goal_xy[2 * k + 1], nk, off};
+        off += nk;
         reqs.push_back(r);
         bs.push_back(r.b);
     }
-    if (off > 0 && !tracks) return fail(c, TWG_E_INVALID_ARG, "null tracks");
-    st = encode(c, reqs, tracks, warp, rcfg->warm_start);
+    if (off > 0 && !tracks && !resident) return fail(c, TWG_E_INVALID_ARG, "null tracks");
+    st = encode(c, reqs, tracks, warp, rcfg->warm_start, resident);
     if (st != TWG_OK) return st;
     std::vector<int> part(c->B, 0);
     for (int q : bs) part[q] = 1;
@@ -880,6 +896,196 @@ TWG_API twg_status twg_get_warp(twg_ctx* c, int32_t b, int32_t n, int32_t* t, in
     if (t) TWG_CUDA(c, cudaMemcpyAsync(t, c->d_t + o, n * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (j) TWG_CUDA(c, cudaMemcpyAsync(j, c->d_j + o, n * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (pred) TWG_CUDA(c, cudaMemcpyAsync(pred, c->d_pred + 3 * o, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_track_update(twg_ctx* c, int32_t b, const double* det_xy, const int32_t* n_det,
+                                    const twg_warp_cfg* wc, const twg_tracker_cfg* cfg, int32_t* n_tracks) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!n_det || !wc || !cfg || b < -1 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    if (!(cfg->sigma_z >= 0.0) || !(cfg->gate >= 0.0) || !(cfg->spawn_var_pos >= 0.0) || !(cfg->spawn_var_vel >= 0.0) ||
+        cfg->prune_after < 0 || cfg->max_tracks < 0)
+        return fail(c, TWG_E_INVALID_ARG, "tracker cfg: sigma_z, gate, variances >= 0, prune_after, max_tracks >= 0");
+    const int nreq = b < 0 ? c->B : 1;
+    std::vector<TrkReq> rq(nreq);
+    int64_t total = 0;
+    int max_n = 0, max_m = 0, need_cap = 1;
+    for (int k = 0; k < nreq; ++k) {
+        if (n_det[k] < 0) return fail(c, TWG_E_INVALID_ARG, "negative detection count");
+        rq[k].b = b < 0 ? k : b;
+        rq[k].n = c->scen[rq[k].b].trk_n;
+        rq[k].m = n_det[k];
+        rq[k].det_off = total;
+        total += n_det[k];
+        max_n = std::max(max_n, rq[k].n);
+        max_m = std::max(max_m, rq[k].m);
+        need_cap = std::max(need_cap, rq[k].n + rq[k].m);
+    }
+    if (total > 0 && !det_xy) return fail(c, TWG_E_INVALID_ARG, "null detections");
+    st = ensure_track_cap(c, need_cap);
+    if (st != TWG_OK) return st;
+    for (int k = 0; k < nreq; ++k)
+        rq[k].limit = cfg->max_tracks > 0 ? std::min(cfg->max_tracks, c->track_cap) : c->track_cap;
+    // scratch: [B][cap] tables, [nreq][mcap] flags, [nreq][pcap] pairs, control words, requests, detections
+    if (c->trk_scratch_cap < c->track_cap) {
+        for (void* p : {(void*)c->d_trk_pred, (void*)c->d_trk_misn, (void*)c->d_trk_match})
+            if (p) cudaFree(p);
+        c->d_trk_pred = nullptr;
+        c->d_trk_misn = c->d_trk_match = nullptr;
+        TWG_CUDA(c, dev_alloc(&c->d_trk_pred, (size_t)c->B * c->track_cap));
+        TWG_CUDA(c, dev_alloc(&c->d_trk_misn, (size_t)c->B * c->track_cap));
+        TWG_CUDA(c, dev_alloc(&c->d_trk_match, (size_t)c->B * c->track_cap));
+        c->trk_scratch_cap = c->track_cap;
+    }
+    int pcap = 4096;
+    while (pcap < 4 * (max_n + max_m)) pcap <<= 1;
+    pcap = std::max(pcap, c->trk_pcap);
+    const int mcap = std::max(max_m, 1);
+    auto alloc_req_scratch = [&](int pc) -> twg_status {
+        if (c->trk_nreq_cap < nreq || c->trk_mcap < mcap) {
+            if (c->d_trk_used) cudaFree(c->d_trk_used);
+            c->d_trk_used = nullptr;
+            TWG_CUDA(c, dev_alloc(&c->d_trk_used, (size_t)std::max(nreq, c->trk_nreq_cap) * std::max(mcap, c->trk_mcap)));
+            c->trk_mcap = std::max(mcap, c->trk_mcap);
+        }
+        if (c->trk_nreq_cap < nreq || c->trk_pcap < pc) {
+            if (c->d_trk_pairs) cudaFree(c->d_trk_pairs);
+            c->d_trk_pairs = nullptr;
+            TWG_CUDA(c, dev_alloc(&c->d_trk_pairs, (size_t)std::max(nreq, c->trk_nreq_cap) * std::max(pc, c->trk_pcap)));
+            c->trk_pcap = std::max(pc, c->trk_pcap);
+        }
+        if (c->trk_nreq_cap < nreq) {
+            if (c->d_trk_ctl) cudaFree(c->d_trk_ctl);
+            if (c->d_trk_req) cudaFree(c->d_trk_req);
+            c->d_trk_ctl = nullptr;
+            c->d_trk_req = nullptr;
+            TWG_CUDA(c, dev_alloc(&c->d_trk_ctl, (size_t)3 * nreq));
+            TWG_CUDA(c, dev_alloc(&c->d_trk_req, (size_t)nreq));
+            c->trk_nreq_cap = nreq;
+        }
+        return TWG_OK;
+    };
+    st = alloc_req_scratch(pcap);
+    if (st != TWG_OK) return st;
+    // detections -> device (double2)
+    const double2* det = nullptr;
+    if (total > 0) {
+        if (is_device_ptr(det_xy) && (reinterpret_cast<uintptr_t>(det_xy) & 15) == 0) {
+            det = reinterpret_cast<const double2*>(det_xy);
+        } else {
+            if (c->trk_det_cap < total) {
+                if (c->d_trk_det) cudaFree(c->d_trk_det);
+                c->d_trk_det = nullptr;
+                TWG_CUDA(c, dev_alloc(&c->d_trk_det, (size_t)total));
+                c->trk_det_cap = total;
+            }
+            if (is_device_ptr(det_xy)) {
+                TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_det, det_xy, (size_t)total * sizeof(double2),
+                                            cudaMemcpyDeviceToDevice, c->stream));
+            } else {
+                void* hd = nullptr;
+                TWG_CUDA(c, stage_alloc(c, (size_t)total * sizeof(double2), &hd));
+                std::memcpy(hd, det_xy, (size_t)total * sizeof(double2));
+                TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_det, hd, (size_t)total * sizeof(double2), cudaMemcpyHostToDevice,
+                                            c->stream));
+            }
+            det = c->d_trk_det;
+        }
+    }
+    TrackArgs t;
+    t.trk = c->d_tracks;
+    t.missed = c->d_missed;
+    t.pred = c->d_trk_pred;
+    t.mis_new = c->d_trk_misn;
+    t.match = c->d_trk_match;
+    t.det = det;
+    t.cap = c->track_cap;
+    t.mcap = c->trk_mcap;
+    t.prune_after = cfg->prune_after;
+    std::memcpy(t.Q, wc->Q, sizeof(t.Q));
+    t.dt = wc->dt;
+    t.r2 = cfg->sigma_z * cfg->sigma_z;
+    t.gate2 = cfg->gate * cfg->gate;
+    t.var_pos = cfg->spawn_var_pos;
+    t.var_vel = cfg->spawn_var_vel;
+    std::vector<int> result_n(nreq, 0);
+    int worst = 0;
+    std::vector<TrkReq> todo = rq;
+    std::vector<int> todo_idx(nreq);
+    for (int k = 0; k < nreq; ++k) todo_idx[k] = k;
+    for (int attempt = 0; !todo.empty(); ++attempt) {
+        const int nr = (int)todo.size();
+        int mn = 0, mm = 0;
+        for (const TrkReq& r : todo) {
+            mn = std::max(mn, r.n);
+            mm = std::max(mm, r.m);
+        }
+        void* hq = nullptr;
+        TWG_CUDA(c, stage_alloc(c, nr * sizeof(TrkReq), &hq));
+        std::memcpy(hq, todo.data(), nr * sizeof(TrkReq));
+        TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_req, hq, nr * sizeof(TrkReq), cudaMemcpyHostToDevice, c->stream));
+        TWG_CUDA(c, cudaMemsetAsync(c->d_trk_ctl, 0, 3 * nr * sizeof(int), c->stream));
+        t.req = c->d_trk_req;
+        t.used = c->d_trk_used;
+        t.pairs = c->d_trk_pairs;
+        t.pcap = c->trk_pcap;
+        t.pcount = c->d_trk_ctl;
+        t.flags = c->d_trk_ctl + nr;
+        t.n_out = c->d_trk_ctl + 2 * nr;
+        int nl = 0;
+        TWG_CUDA(c, launch_track_step(t, nr, mn, mm, &nl, c->stream));
+        c->launches += nl;
+        int* hc = nullptr;
+        TWG_CUDA(c, stage_alloc(c, 3 * nr * sizeof(int), reinterpret_cast<void**>(&hc)));
+        TWG_CUDA(c, cudaMemcpyAsync(hc, c->d_trk_ctl, 3 * nr * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+        std::vector<TrkReq> again;
+        std::vector<int> again_idx;
+        int need = 0;
+        for (int q = 0; q < nr; ++q) {
+            const int fl = hc[nr + q];
+            if (fl & kTrkOverflow) {  // more gated pairs than the list holds: grow and redo this scenario
+                again.push_back(todo[q]);
+                again_idx.push_back(todo_idx[q]);
+                need = std::max(need, hc[q]);
+                continue;
+            }
+            result_n[todo_idx[q]] = hc[2 * nr + q];
+            c->scen[todo[q].b].trk_n = hc[2 * nr + q];
+            if (fl & kTrkSingular) worst = std::max(worst, (int)TWG_W_SINGULAR_INNOVATION);
+            if (fl & kTrkTruncated) worst = std::max(worst, (int)TWG_W_TRUNCATED);
+        }
+        if (!again.empty()) {
+            if (attempt > 40) return fail(c, TWG_E_NO_MEMORY, "tracker pair list cannot grow");
+            int pc = c->trk_pcap;
+            while (pc < need) pc <<= 1;
+            st = alloc_req_scratch(pc);
+            if (st != TWG_OK) return st;
+        }
+        todo.swap(again);
+        todo_idx.swap(again_idx);
+    }
+    if (n_tracks)
+        for (int k = 0; k < nreq; ++k) n_tracks[k] = result_n[k];
+    return (twg_status)worst;
+}
+
+TWG_API twg_status twg_get_tracks(twg_ctx* c, int32_t b, twg_track* out, int32_t* missed, int32_t cap, int32_t* n) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (b < 0 || b >= c->B || cap < 0) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    const int nt = c->scen[b].trk_n;
+    if (n) *n = nt;
+    const int k = std::min(cap, nt);
+    if (k > 0) {
+        const int64_t o = (int64_t)b * c->track_cap;
+        if (out)
+            TWG_CUDA(c, cudaMemcpyAsync(out, c->d_tracks + o, k * sizeof(twg_track), cudaMemcpyDefault, c->stream));
+        if (missed)
+            TWG_CUDA(c, cudaMemcpyAsync(missed, c->d_missed + o, k * sizeof(int), cudaMemcpyDefault, c->stream));
+    }
     TWG_CUDA(c, cudaStreamSynchronize(c->stream));
     return TWG_OK;
 }

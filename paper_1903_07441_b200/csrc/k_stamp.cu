@@ -198,12 +198,15 @@ __global__ void k_set_goal(EncodeArgs e) {
 }
 
 __global__ void k_scatter_tracks(const twg_track* __restrict__ src, const int* __restrict__ off, int nscen,
-                                 const int* __restrict__ scen_b, twg_track* __restrict__ dst, int cap) {
+                                 const int* __restrict__ scen_b, twg_track* __restrict__ dst, int* __restrict__ missed,
+                                 int cap) {
     const int k = blockIdx.y;
     if (k >= nscen) return;
     const int n = off[k + 1] - off[k];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         dst[(int64_t)scen_b[k] * cap + i] = src[off[k] + i];
+        missed[(int64_t)scen_b[k] * cap + i] = 0;  // caller-supplied tracks replace the tracker table (f1)
+    }
 }
 
 // Fresh context: every cell free at 0.5, pad columns fixed obstacles.
@@ -254,8 +257,8 @@ cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P,
 }
 
 cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nscen, const int* scen_b, twg_track* dst,
-                                  int cap, cudaStream_t st) {
-    k_scatter_tracks<<<dim3(1, nscen), 128, 0, st>>>(src, off, nscen, scen_b, dst, cap);
+                                  int* missed, int cap, cudaStream_t st) {
+    k_scatter_tracks<<<dim3(1, nscen), 128, 0, st>>>(src, off, nscen, scen_b, dst, missed, cap);
     return cudaGetLastError();
 }
 

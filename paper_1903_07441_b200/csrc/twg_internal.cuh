@@ -63,6 +63,13 @@ struct WarpCfgDev {
     int fmode;  // 0: predicted covariance (C19); 1: posterior covariance (C27)
 };
 
+struct TrkReq {  // one scenario of a tracker tick (row f1)
+    int b;            // scenario
+    int n, m;         // tracks before the tick, detections
+    int limit;        // track capacity after the tick
+    int64_t det_off;  // first detection in TrackArgs::det
+};
+
 struct PathMeta {  // per scenario, written by k_walk / k_band
     int n_cells;
     int status;
@@ -150,6 +157,7 @@ struct twg_ctx {
     struct Scen {
         int gx = -1, gy = -1, rcx = -1, rcy = -1;
         int n_tracks = 0, n_boxes = 0;
+        int trk_n = 0;  // tracks in the resident tracker table (row f1)
         bool encoded = false, static_dirty = true;
     };
     std::vector<Scen> scen;
@@ -159,6 +167,19 @@ struct twg_ctx {
     int* d_j = nullptr;
     double* d_pred = nullptr;          // [B][cap][3]
     int4* d_boxes = nullptr;           // [B][cap] (x0, x1, y0, y1) inclusive; empty if x0 > x1
+    int* d_missed = nullptr;           // [B][cap] tracker missed counters (row f1)
+    // tracker scratch (row f1)
+    int trk_scratch_cap = 0;           // per-scenario capacity of the [B][cap] scratch tables
+    twg_track* d_trk_pred = nullptr;
+    int* d_trk_misn = nullptr;
+    int* d_trk_match = nullptr;
+    int trk_mcap = 0, trk_pcap = 0, trk_nreq_cap = 0;
+    uint8_t* d_trk_used = nullptr;     // [nreq][mcap]
+    ulonglong2* d_trk_pairs = nullptr; // [nreq][pcap]
+    int* d_trk_ctl = nullptr;          // [3][nreq]: pair count, flags, tracks out
+    twg::TrkReq* d_trk_req = nullptr;
+    double2* d_trk_det = nullptr;
+    int64_t trk_det_cap = 0;
     twg::ScenParams* d_params = nullptr;
     int params_cap = 0;
     twg::WarpCfgDev* d_wcfg = nullptr;

@@ -42,7 +42,28 @@ struct EncodeArgs {
 cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_tracks, int any_cold, int* n_launch,
                           cudaStream_t st);
 cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nscen, const int* scen_b, twg_track* dst,
-                                  int cap, cudaStream_t st);
+                                  int* missed, int cap, cudaStream_t st);
+
+// k_track.cu (row f1: tracker tick)
+enum : int { kTrkTruncated = 1, kTrkSingular = 2, kTrkOverflow = 4 };
+struct TrackArgs {
+    twg_track* trk;        // [B][cap] resident table (= the encode track table)
+    int* missed;           // [B][cap]
+    twg_track* pred;       // [B][cap] scratch
+    int* mis_new;          // [B][cap] scratch
+    int* match;            // [B][cap] detection matched to each track, or -1
+    uint8_t* used;         // [nreq][mcap] detection matched
+    const double2* det;    // concatenated detections (x, y)
+    const TrkReq* req;     // [nreq]
+    ulonglong2* pairs;     // [nreq][pcap] gated pairs (d^2 bits, track << 32 | detection)
+    int* pcount;           // [nreq]
+    int* flags;            // [nreq]
+    int* n_out;            // [nreq]
+    int cap, mcap, pcap;   // pcap: power of two
+    int prune_after;
+    double Q[16], dt, r2, gate2, var_pos, var_vel;
+};
+cudaError_t launch_track_step(const TrackArgs& t, int nreq, int max_n, int max_m, int* n_launch, cudaStream_t st);
 
 // k_path.cu (rows a7-a9)
 struct PathArgs {
@@ -72,5 +93,6 @@ cudaError_t launch_index_dir(const PathArgs& p, cudaStream_t st);  // k_index_di
 void preload_relax_kernels();
 void preload_stamp_kernels();
 void preload_path_kernels();
+void preload_track_kernels();
 
 }  // namespace twg

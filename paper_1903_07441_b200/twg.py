@@ -19,6 +19,8 @@ LIB_PATH = os.path.join(_HERE, "libtwg.so")
 OK, W_GOAL_SWALLOWED, W_TRUNCATED = 0, 1, 2
 E_INVALID_ARG, E_OUT_OF_BOUNDS, E_OVERLAPPING_CLASSES, E_INVALID_START = -1, -2, -3, -4
 E_NO_PATH, E_CUDA, E_NCCL, E_NO_MEMORY = -5, -6, -7, -8
+W_SINGULAR_INNOVATION = 3
+RESIDENT_TRACKS = -1
 
 
 class GridDesc(C.Structure):
@@ -52,6 +54,11 @@ class BandCfg(C.Structure):
                 ("reserved", C.c_int32), ("step", C.c_float), ("k_t", C.c_float)]
 
 
+class TrackerCfg(C.Structure):
+    _fields_ = [("sigma_z", C.c_double), ("gate", C.c_double), ("spawn_var_pos", C.c_double),
+                ("spawn_var_vel", C.c_double), ("prune_after", C.c_int32), ("max_tracks", C.c_int32)]
+
+
 class PlanResult(C.Structure):
     _fields_ = [("status", C.c_int32), ("sweeps", C.c_int32), ("n_cells", C.c_int32), ("n_smooth", C.c_int32),
                 ("residual", C.c_float), ("next_x", C.c_float), ("next_y", C.c_float), ("walk_status", C.c_int32)]
@@ -72,6 +79,8 @@ SIGNATURES = [
     ("twg_get_field", C.c_int32, [_P, C.c_int32, _P, C.c_int32]),
     ("twg_set_field", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_get_warp", C.c_int32, [_P, C.c_int32, C.c_int32, _P, _P, _P]),
+    ("twg_track_update", C.c_int32, [_P, C.c_int32, _P, _P, C.POINTER(WarpCfg), C.POINTER(TrackerCfg), _P]),
+    ("twg_get_tracks", C.c_int32, [_P, C.c_int32, _P, _P, C.c_int32, C.POINTER(C.c_int32)]),
     ("twg_index_matrix", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_warp_map", C.c_int32, [_P, C.POINTER(Robot), C.c_double, _P]),
     ("twg_field_ptr", C.c_int32, [_P, C.c_int32, C.POINTER(_P), C.POINTER(C.c_int64)]),
@@ -146,6 +155,10 @@ def relax_cfg(max_sweeps=100, check_every=0, warm_start=1, temporal_depth=0, tol
     return RelaxCfg(max_sweeps, check_every, warm_start, temporal_depth, tol, rows_per_warp, sync_every, mode)
 
 
+def tracker_cfg(sigma_z=0.05, gate=0.5, spawn_var_pos=0.25, spawn_var_vel=1.0, prune_after=10, max_tracks=0):
+    return TrackerCfg(sigma_z, gate, spawn_var_pos, spawn_var_vel, prune_after, max_tracks)
+
+
 def band_cfg(iterations=50, max_len=4096, max_smooth=8192, step=0.25, k_t=1.0):
     return BandCfg(iterations, max_len, max_smooth, 0, step, k_t)
 
@@ -187,9 +200,13 @@ class Planner:
         return _check(self.ctx, lib().twg_set_static(self.ctx, b, _ptr(occ)))
 
     def set_obstacles(self, b, robot, goal, tracks, cfg, warm=0):
+        """tracks=None: use the resident tracker table (twg_track_update)."""
+        r = Robot(*[float(v) for v in robot])
+        if tracks is None:
+            return _check(self.ctx, lib().twg_set_obstacles(self.ctx, b, C.byref(r), int(goal[0]), int(goal[1]),
+                                                            None, RESIDENT_TRACKS, C.byref(cfg), int(warm)))
         t = tracks if hasattr(tracks, "data_ptr") else tracks_array(tracks)
         n = int(t.shape[0])
-        r = Robot(*[float(v) for v in robot])
         return _check(self.ctx, lib().twg_set_obstacles(self.ctx, b, C.byref(r), int(goal[0]), int(goal[1]),
                                                         _ptr(t) if n else None, n, C.byref(cfg), int(warm)))
 
@@ -220,12 +237,14 @@ class Planner:
         nb = 1 if b >= 0 else self.B
         rob = (Robot * nb)(*[Robot(*[float(v) for v in r]) for r in robots])
         g = np.ascontiguousarray(np.asarray(goals, np.int32).reshape(nb, 2))
-        nt = np.ascontiguousarray(np.asarray(n_tracks, np.int32).reshape(nb))
-        t = tracks if hasattr(tracks, "data_ptr") else tracks_array(tracks)
+        resident = tracks is None and n_tracks is None
+        nt = None if resident else np.ascontiguousarray(np.asarray(n_tracks, np.int32).reshape(nb))
+        t = None if resident else (tracks if hasattr(tracks, "data_ptr") else tracks_array(tracks))
         out = (PlanResult * nb)()
         cells = np.zeros((nb, bcfg.max_len, 2), np.int32) if want_paths else None
         sm = np.zeros((nb, bcfg.max_smooth, 2), np.float32) if want_paths else None
-        st = lib().twg_plan_step(self.ctx, b, rob, _ptr(g), _ptr(t) if int(nt.sum()) else None, _ptr(nt),
+        st = lib().twg_plan_step(self.ctx, b, rob, _ptr(g), _ptr(t) if (nt is not None and int(nt.sum())) else None,
+                                 _ptr(nt),
                                  C.byref(wcfg), C.byref(rcfg), C.byref(bcfg), out, _ptr(cells), _ptr(sm))
         _check(self.ctx, st, ok=(OK, W_GOAL_SWALLOWED, W_TRUNCATED, E_NO_PATH))
         return st, list(out), cells, sm
@@ -246,6 +265,27 @@ class Planner:
         pred = np.zeros((max(n, 1), 3))
         _check(self.ctx, lib().twg_get_warp(self.ctx, b, n, _ptr(t), _ptr(j), _ptr(pred)))
         return t[:n], j[:n], pred[:n]
+
+    # -- f1 tracker
+    def track_update(self, b, det, n_det, wcfg, tcfg):
+        """twg_track_update: det [sum n_det, 2] float64 (numpy or CUDA tensor); returns (status, n_tracks)."""
+        nb = 1 if b >= 0 else self.B
+        nd = np.ascontiguousarray(np.asarray(n_det, np.int32).reshape(nb))
+        d = det if hasattr(det, "data_ptr") else np.ascontiguousarray(np.asarray(det, np.float64).reshape(-1, 2))
+        nt = np.zeros(nb, np.int32)
+        st = lib().twg_track_update(self.ctx, b, _ptr(d) if int(nd.sum()) else None, _ptr(nd), C.byref(wcfg),
+                                    C.byref(tcfg), _ptr(nt))
+        _check(self.ctx, st, ok=(OK, W_TRUNCATED, W_SINGULAR_INNOVATION))
+        return st, nt
+
+    def get_tracks(self, b=0):
+        """twg_get_tracks: (tracks [n, 20] float64, missed [n] int32) of the resident table."""
+        n = C.c_int32()
+        _check(self.ctx, lib().twg_get_tracks(self.ctx, b, None, None, 0, C.byref(n)))
+        out = np.zeros((max(n.value, 1), 20))
+        mis = np.zeros(max(n.value, 1), np.int32)
+        _check(self.ctx, lib().twg_get_tracks(self.ctx, b, _ptr(out), _ptr(mis), n.value, C.byref(n)))
+        return out[: n.value], mis[: n.value]
 
     def index_matrix(self, b=0, out=None):
         """twg_index_matrix: uint8 [H, W] M_idx of scenario b (0..3 move, 4 goal, 5 obstacle, 6 none)."""
