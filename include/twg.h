@@ -168,6 +168,34 @@ typedef struct {
 /* n / n_tracks value selecting the context's resident tracker table. */
 #define TWG_RESIDENT_TRACKS (-1)
 
+/* Closed-loop simulator (row f2; C31-C36), defaults in brackets:
+ *   dt [0.1 s]; robot_radius, obstacle_radius [0.25 m]; goal_radius [0.3 m];
+ *   turn_distance [0.5 m] obstacles turn away from walls / obstacles this
+ *   far ahead; heading_sigma [0.02 rad] obstacle heading jitter;
+ *   det_sigma [0.05 m] detection noise; turn_max [9 deg = 90 deg/s
+ *   at dt 0.1] robot turn per tick; seed of the counter-based
+ *   generator (C31); max_ticks [1000] trial time limit; init_tol [1e-6],
+ *   init_max_sweeps [1e6]: the tick-0 field is relaxed to this residual
+ *   (Alg. 1 "Initialize ... harmonic potential values"; C36). */
+typedef struct {
+    double dt, robot_radius, obstacle_radius, goal_radius, turn_distance, heading_sigma, det_sigma, turn_max;
+    uint64_t seed;
+    int32_t max_ticks, init_max_sweeps;
+    float init_tol;
+    int32_t reserved;
+} twg_sim_cfg;
+
+/* State of one trial. status: 0 running, 1 success (robot centre within
+ * goal_radius of the goal cell centre), 2 collision (robot centre outside
+ * the grid, a static wall cell centre within robot_radius, or an obstacle
+ * closer than robot_radius + obstacle_radius), 3 timeout,
+ * 4 idle (never reset).  (hx, hy): unit heading; length: distance
+ * travelled (m). */
+typedef struct {
+    double x, y, hx, hy, speed, length;
+    int32_t ticks, status;
+} twg_sim_trial;
+
 /* Result of one planning tick.  next_x/next_y: next waypoint in cell units
  * (cell (i, k) has centre (i + 0.5, k + 0.5)) (Alg. 1). */
 typedef struct {
@@ -297,6 +325,33 @@ TWG_API twg_status twg_track_update(twg_ctx* ctx, int32_t b, const double* det_x
  * their missed counters into missed (host or device; either may be NULL);
  * *n = the table's track count. */
 TWG_API twg_status twg_get_tracks(twg_ctx* ctx, int32_t b, twg_track* out, int32_t* missed, int32_t cap, int32_t* n);
+
+/* Row f2: start trial b of the closed-loop simulator.  robot: start pose
+ * and constant speed (the robot never stops); goal cell;
+ * obstacles[n][4] = (x, y, vx, vy) true states (host), constant speed
+ * sqrt(vx^2 + vy^2).  Clears b's tracker table, encodes the static map and
+ * goal cold and relaxes that field to cfg->init_tol (C36), and produces the
+ * tick-0 detections.  Errors: INVALID_ARG, OUT_OF_BOUNDS, INVALID_START,
+ * OVERLAPPING_CLASSES (as twg_set_obstacles), CUDA. */
+TWG_API twg_status twg_sim_reset(twg_ctx* ctx, int32_t b, const twg_robot* robot, int32_t goal_x, int32_t goal_y,
+                                 const double* obstacles, int32_t n, const twg_sim_cfg* cfg);
+
+/* Row f2: one tick of every running trial -- Algorithm 1 closed loop
+ * (P:674-709): tracker tick on the current detections (row f1), Map Update
+ * from the resident tracks (a1-a3, robot heading theta = atan2(hy, hx)),
+ * relaxation (a4-a6), path (a7-a9), then the simulator step (robot toward
+ * the next waypoint, or straight on when no path exists; obstacles
+ * move; status) and the next tick's detections.  out[batch] (host, may be
+ * NULL) receives every trial's state, *running the number still running.
+ * Returns the worst planner status of the tick (warnings >= 0) or an
+ * error. */
+TWG_API twg_status twg_sim_tick(twg_ctx* ctx, const twg_sim_cfg* cfg, const twg_warp_cfg* warp,
+                                const twg_relax_cfg* relax, const twg_band_cfg* band, const twg_tracker_cfg* tracker,
+                                twg_sim_trial* out, int32_t* running);
+
+/* Row f2: trial b's turning-angle histogram, hist[36] (bin k: per-tick
+ * heading change in [5k, 5k + 5) degrees), host. */
+TWG_API twg_status twg_sim_histogram(twg_ctx* ctx, int32_t b, int32_t* hist);
 
 /* Full-grid index matrix M_idx of scenario b's current field (Eq. 3,
  * P:228-233; Alg. 1): out[height x width] uint8

@@ -79,6 +79,16 @@ def lib():
         L.orc_associate.argtypes = [i32, P, i32, P, d, P, P]
         L.orc_track_step.restype = i32
         L.orc_track_step.argtypes = [i32, P, P, i32, i32, P, d, P, d, d, d, d, i32, i32, P]
+        u64 = C.c_uint64
+        L.orc_rng_u01.restype = d
+        L.orc_rng_u01.argtypes = [u64, u64, u64, u64, u64]
+        L.orc_rng_normal.restype = d
+        L.orc_rng_normal.argtypes = [u64, u64, u64, u64, u64]
+        L.orc_sim_sense.restype = None
+        L.orc_sim_sense.argtypes = [i32, P, d, u64, u64, u64, P]
+        L.orc_sim_move.restype = None
+        L.orc_sim_move.argtypes = [i32, i32, d, d, d, P, P, P, P, d, d, i32, d, d, i32, P, P, P, i32, u64, u64,
+                                   P, P]
         L.orc_warp_map.restype = None
         L.orc_warp_map.argtypes = [i32, i32, d, d, d, d, d, d, d, P]
         L.orc_init_u32.restype = None
@@ -394,3 +404,88 @@ def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0
     else:
         out.update(band=np.zeros((0, 2), np.float32), smooth=np.zeros((0, 2), np.float32), next=None)
     return out
+
+
+# ----------------------------------------------------------------------------- f2 simulator
+SIM_RUNNING, SIM_SUCCESS, SIM_COLLISION, SIM_TIMEOUT = 0, 1, 2, 3
+
+
+def rng_u01(seed, trial, tick, entity, k):
+    return lib().orc_rng_u01(seed, trial, tick, entity, k)
+
+
+def rng_normal(seed, trial, tick, entity, stream):
+    return lib().orc_rng_normal(seed, trial, tick, entity, stream)
+
+
+def sim_sense(obs, sigma_z, seed, trial, tick):
+    obs = np.ascontiguousarray(obs, np.float64).reshape(-1, 4)
+    z = np.zeros((max(len(obs), 1), 2))
+    lib().orc_sim_sense(len(obs), _p(obs), float(sigma_z), seed, trial, tick, _p(z))
+    return z[: len(obs)].copy()
+
+
+def sim_cos_bins():
+    """cos(5 k degrees), k = 0..36: the turning-angle histogram thresholds (C35)."""
+    return np.array([math.cos(k * 5.0 * math.pi / 180.0) for k in range(37)], np.float64)
+
+
+class SimState:
+    """One trial: robot [x, y, hx, hy, speed, length], ticks, status, obstacles [n, 4], speeds, histogram."""
+
+    def __init__(self, scene, cfg):
+        xr, yr, th, sp = scene.robot
+        self.rob = np.array([xr, yr, math.cos(th), math.sin(th), sp, 0.0])
+        self.ticks = np.zeros(1, np.int32)
+        self.status = np.zeros(1, np.int32)
+        self.obs = np.ascontiguousarray(scene.truth, np.float64).reshape(-1, 4).copy()
+        self.speed = np.sqrt(self.obs[:, 2] * self.obs[:, 2] + self.obs[:, 3] * self.obs[:, 3])
+        self.hist = np.zeros(36, np.int32)
+        self.goal = (scene.origin[0] + (scene.goal[0] + 0.5) * scene.cell_size,
+                     scene.origin[1] + (scene.goal[1] + 0.5) * scene.cell_size)
+
+
+def sim_move(scene, state, wp, cfg, trial):
+    """One simulator tick (orc_sim_move); wp = (x, y) cell units or None (blocked)."""
+    c = np.array([cfg.dt, cfg.robot_radius, cfg.obstacle_radius, cfg.goal_radius, cfg.turn_distance,
+                  cfg.heading_sigma, math.cos(cfg.turn_max), math.sin(cfg.turn_max)])
+    mask = np.ascontiguousarray(scene.static, np.uint8)
+    bins = sim_cos_bins()
+    has = 0 if wp is None else 1
+    wx, wy = (0.0, 0.0) if wp is None else (float(wp[0]), float(wp[1]))
+    lib().orc_sim_move(scene.W, scene.H, scene.cell_size, scene.origin[0], scene.origin[1], _p(mask),
+                       _p(state.rob), _p(state.ticks), _p(state.status), state.goal[0], state.goal[1], has, wx, wy,
+                       len(state.obs), _p(state.obs), _p(state.speed), _p(c), int(cfg.max_ticks), cfg.seed, trial,
+                       _p(bins), _p(state.hist))
+
+
+def sim_run(scene, cfg, trial=0, max_ticks=None, sweeps=100, iters=50, max_len=4096, tracker=None, warp_scene=None):
+    """Closed loop of Algorithm 1 on the CPU (sense -> track -> plan -> move), until the trial ends or
+    max_ticks ticks ran.  Returns the final SimState and the per-tick records."""
+    from dataclasses import replace
+    tk = tracker or {}
+    st = SimState(scene, cfg)
+    z = sim_sense(st.obs, cfg.det_sigma, cfg.seed, trial, 0)
+    tracks, missed = np.zeros((0, 20)), np.zeros(0, np.int32)
+    # Alg. 1 "Initialize the 2D map and harmonic potential values" (P:676; C36): the static map and
+    # goal, no tracks, relaxed cold to init_tol (checked every 100 sweeps)
+    _, cls0, *_ = classify(replace(scene, tracks=np.zeros((0, 20))))
+    u0 = init_u32(cls0)
+    init_sweeps, _ = relax_f32(cls0, u0, cfg.init_max_sweeps, 100, cfg.init_tol)
+    prev = {"u": u0, "init_sweeps": init_sweeps}
+    recs = []
+    Q = np.ascontiguousarray(scene.warp.Q, np.float64).reshape(16)
+    lim = cfg.max_ticks if max_ticks is None else max_ticks
+    while st.status[0] == SIM_RUNNING and st.ticks[0] < lim:
+        _, tracks, missed = track_step(tracks, missed, z, dt=scene.warp.dt, Q=Q, **tk)
+        th = math.atan2(st.rob[3], st.rob[2])
+        sc = replace(scene, robot=(float(st.rob[0]), float(st.rob[1]), th, float(st.rob[4])), tracks=tracks)
+        ref = plan_step(sc, max_sweeps=sweeps, iters=iters, max_len=max_len, prev=prev)
+        wp = ref["next"] if ref.get("walk_status", -1) == OK else None
+        sim_move(scene, st, wp, cfg, trial)
+        recs.append({"rob": st.rob.copy(), "obs": st.obs.copy(), "n_tracks": len(tracks), "wp": wp,
+                     "status": int(st.status[0]), "u": ref.get("u")})
+        z = sim_sense(st.obs, cfg.det_sigma, cfg.seed, trial, int(st.ticks[0]))
+        prev = ref
+    st.tracks, st.missed = tracks, missed
+    return st, recs

@@ -816,3 +816,203 @@ int32_t orc_track_step(int32_t n, double* trk, int32_t* missed, int32_t cap, int
     free(pred); free(pxy); free(mt); free(mis); free(du);
     return status;
 }
+
+/* ------------------------------------------------------------------------ */
+/* f2  closed-loop simulator ("Move the robot",       */
+/* P:758-768 the success protocol, P:538-540 obstacle motion;    */
+/* readings C31-C35).  Only + - * / sqrt floor, so the CUDA simulator can   */
+/* be bit-identical; randomness is the counter-based generator below, which */
+/* the CUDA side implements independently.                                  */
+/* ------------------------------------------------------------------------ */
+
+static uint64_t orc_splitmix(uint64_t z)
+{
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+/* Uniform in [0, 1) with 53 random bits, a pure function of the counters (C31). */
+double orc_rng_u01(uint64_t seed, uint64_t trial, uint64_t tick, uint64_t entity, uint64_t k)
+{
+    uint64_t h = orc_splitmix(seed ^ orc_splitmix(trial ^ orc_splitmix(tick ^ orc_splitmix(entity * 64u + k))));
+    return (double)(h >> 11) * 0x1.0p-53;
+}
+
+/* Approximately standard normal: Irwin-Hall sum of 12 uniforms minus 6 (C31). */
+double orc_rng_normal(uint64_t seed, uint64_t trial, uint64_t tick, uint64_t entity, uint64_t stream)
+{
+    double s = 0.0;
+    for (uint64_t i = 0; i < 12; ++i) s = s + orc_rng_u01(seed, trial, tick, entity, stream * 16u + i);
+    return s - 6.0;
+}
+
+/* Detections of tick `tick` (C32): every obstacle, in index order, at its true position plus
+ * sigma_z N(0,1) per axis (streams 1, 2). z[2 n]. */
+void orc_sim_sense(int32_t n, const double* obs, double sigma_z, uint64_t seed, uint64_t trial, uint64_t tick,
+                   double* z)
+{
+    for (int32_t i = 0; i < n; ++i) {
+        z[2 * i] = obs[4 * i] + sigma_z * orc_rng_normal(seed, trial, tick, (uint64_t)i, 1);
+        z[2 * i + 1] = obs[4 * i + 1] + sigma_z * orc_rng_normal(seed, trial, tick, (uint64_t)i, 2);
+    }
+}
+
+static int orc_blocked(int32_t W, int32_t H, double cs, double ox, double oy, const uint8_t* mask, double px,
+                       double py)
+{
+    double fx = floor((px - ox) / cs), fy = floor((py - oy) / cs);
+    if (!(fx >= 0.0 && fy >= 0.0 && fx < (double)W && fy < (double)H)) return 1;
+    return mask[(size_t)fy * W + (size_t)fx] != 0;
+}
+
+/* Any sample p + (k / m) td u, k = 1..m, m = ceil(td / (cs / 2)), blocked (C34: thin walls are
+ * not jumped over). */
+static int orc_probe(int32_t W, int32_t H, double cs, double ox, double oy, const uint8_t* mask, double x,
+                     double y, double ux, double uy, double td)
+{
+    int32_t m = (int32_t)ceil(td / (0.5 * cs));
+    for (int32_t k = 1; k <= m; ++k) {
+        double d = td * (double)k / (double)m;
+        if (orc_blocked(W, H, cs, ox, oy, mask, x + ux * d, y + uy * d)) return 1;
+    }
+    return 0;
+}
+
+/* One simulator tick for one trial (C33-C35), after the planner produced waypoint (wp_x, wp_y)
+ * in cell units (has_wp = 0: the walk failed -- the robot keeps its heading):
+ *   robot: heading turns toward the waypoint by at most the angle whose cosine/sine are
+ *     cfg[6], cfg[7], renormalised; position advances speed dt (never stops);
+ *     turning-angle histogram bin k: the largest k with dot(h_old, h_new) <= cos_bins[k];
+ *   obstacles (Jacobi: every rule reads the tick-start positions): heading jitter by the
+ *     rational (Cayley) rotation with a = sigma_h N / 2 (stream 0); turn away from the first
+ *     other obstacle within 2 r_o + turn_dist that lies ahead (reflection about the centre
+ *     line); turn away from walls probed up to turn_dist ahead per axis (orc_probe;
+ *     reflection), speed restored,
+ *     move v dt, clamp into [r_o, extent - r_o];
+ *   status: collision (robot centre outside the grid, a wall cell centre within r_r, or an
+ *     obstacle centre closer than r_r + r_o) before success (within goal_r of the goal); then
+ *     timeout at max_ticks (P:758-763 strict criterion).
+ * rob[6] = x, y, hx, hy, speed, length; obs[n][4] = x, y, vx, vy; obs_speed[n];
+ * cfg = dt, r_robot, r_obs, goal_r, turn_dist, sigma_h, cos_d, sin_d. */
+void orc_sim_move(int32_t W, int32_t H, double cs, double ox, double oy, const uint8_t* mask, double* rob,
+                  int32_t* ticks, int32_t* status, double goal_x, double goal_y, int32_t has_wp, double wp_x,
+                  double wp_y, int32_t n, double* obs, const double* obs_speed, const double* cfg,
+                  int32_t max_ticks, uint64_t seed, uint64_t trial, const double* cos_bins, int32_t* hist)
+{
+    const double dt = cfg[0], rr = cfg[1], ro = cfg[2], gr = cfg[3], td = cfg[4], sh = cfg[5];
+    const double cd = cfg[6], sd = cfg[7];
+    const uint64_t tick = (uint64_t)*ticks;
+    /* robot */
+    double hx = rob[2], hy = rob[3];
+    double nhx = hx, nhy = hy;
+    if (has_wp) {
+        double dx = (ox + wp_x * cs) - rob[0];
+        double dy = (oy + wp_y * cs) - rob[1];
+        double l2 = dx * dx + dy * dy;
+        if (l2 > 0.0) {
+            double l = sqrt(l2);
+            double ux = dx / l, uy = dy / l;
+            double dot = hx * ux + hy * uy;
+            if (dot >= cd) {
+                nhx = ux;
+                nhy = uy;
+            } else {
+                double sg = (hx * uy - hy * ux) >= 0.0 ? 1.0 : -1.0;
+                nhx = hx * cd - sg * (hy * sd);
+                nhy = sg * (hx * sd) + hy * cd;
+            }
+            double nn = sqrt(nhx * nhx + nhy * nhy);
+            nhx = nhx / nn;
+            nhy = nhy / nn;
+        }
+    }
+    double dturn = hx * nhx + hy * nhy;
+    int32_t bin = 0;
+    for (int32_t k = 35; k >= 0; --k)
+        if (dturn <= cos_bins[k]) { bin = k; break; }
+    hist[bin] += 1;
+    const double step = rob[4] * dt;
+    rob[0] = rob[0] + step * nhx;
+    rob[1] = rob[1] + step * nhy;
+    rob[2] = nhx;
+    rob[3] = nhy;
+    rob[5] = rob[5] + step;
+    /* obstacles, from the tick-start positions */
+    double* old = (double*)malloc(sizeof(double) * 4 * (size_t)(n > 0 ? n : 1));
+    memcpy(old, obs, sizeof(double) * 4 * (size_t)n);
+    const double xmax = ox + (double)W * cs, ymax = oy + (double)H * cs;
+    for (int32_t i = 0; i < n; ++i) {
+        double x = old[4 * i], y = old[4 * i + 1], vx = old[4 * i + 2], vy = old[4 * i + 3];
+        double a = 0.5 * sh * orc_rng_normal(seed, trial, tick, (uint64_t)i, 0);
+        double a2 = a * a;
+        double c = (1.0 - a2) / (1.0 + a2), s = (2.0 * a) / (1.0 + a2);
+        double rvx = c * vx - s * vy, rvy = s * vx + c * vy;
+        vx = rvx;
+        vy = rvy;
+        const double lim = 2.0 * ro + td;
+        for (int32_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double dx = old[4 * j] - x, dy = old[4 * j + 1] - y;
+            double d2 = dx * dx + dy * dy;
+            if (d2 < lim * lim && d2 > 0.0 && dx * vx + dy * vy > 0.0) {
+                double d = sqrt(d2);
+                double nx = dx / d, ny = dy / d;
+                double vn = vx * nx + vy * ny;
+                vx = vx - 2.0 * vn * nx;
+                vy = vy - 2.0 * vn * ny;
+                break;
+            }
+        }
+        double vs = sqrt(vx * vx + vy * vy);
+        if (vs > 0.0) {
+            double ux = vx / vs, uy = vy / vs;
+            int bx = orc_probe(W, H, cs, ox, oy, mask, x, y, ux, 0.0, td);
+            int by = orc_probe(W, H, cs, ox, oy, mask, x, y, 0.0, uy, td);
+            if (bx) vx = -vx;
+            if (by) vy = -vy;
+            if (!bx && !by && orc_probe(W, H, cs, ox, oy, mask, x, y, ux, uy, td)) {
+                vx = -vx;
+                vy = -vy;
+            }
+            double f = obs_speed[i] / vs;
+            vx = vx * f;
+            vy = vy * f;
+        }
+        x = x + vx * dt;
+        y = y + vy * dt;
+        if (x < ox + ro) { x = ox + ro; vx = fabs(vx); }
+        if (x > xmax - ro) { x = xmax - ro; vx = -fabs(vx); }
+        if (y < oy + ro) { y = oy + ro; vy = fabs(vy); }
+        if (y > ymax - ro) { y = ymax - ro; vy = -fabs(vy); }
+        obs[4 * i] = x;
+        obs[4 * i + 1] = y;
+        obs[4 * i + 2] = vx;
+        obs[4 * i + 3] = vy;
+    }
+    free(old);
+    /* status */
+    const double x = rob[0], y = rob[1];
+    int coll = !(x >= ox && y >= oy && x < xmax && y < ymax);
+    if (!coll) {
+        int32_t cx0 = (int32_t)floor((x - rr - ox) / cs), cx1 = (int32_t)floor((x + rr - ox) / cs);
+        int32_t cy0 = (int32_t)floor((y - rr - oy) / cs), cy1 = (int32_t)floor((y + rr - oy) / cs);
+        for (int32_t cy = cy0; cy <= cy1 && !coll; ++cy)
+            for (int32_t cx = cx0; cx <= cx1 && !coll; ++cx) {
+                if (cx < 0 || cy < 0 || cx >= W || cy >= H) continue;
+                if (!mask[(size_t)cy * W + cx]) continue;
+                double ddx = (ox + ((double)cx + 0.5) * cs) - x, ddy = (oy + ((double)cy + 0.5) * cs) - y;
+                if (ddx * ddx + ddy * ddy <= rr * rr) coll = 1;
+            }
+    }
+    for (int32_t j = 0; j < n && !coll; ++j) {
+        double dx = obs[4 * j] - x, dy = obs[4 * j + 1] - y;
+        double lim = rr + ro;
+        if (dx * dx + dy * dy < lim * lim) coll = 1;
+    }
+    *ticks = *ticks + 1;
+    if (coll) *status = 2;
+    else if ((x - goal_x) * (x - goal_x) + (y - goal_y) * (y - goal_y) <= gr * gr) *status = 1;
+    else if (*ticks >= max_ticks) *status = 3;
+}

@@ -12,6 +12,7 @@ from .twg import (  # noqa: F401
     relax_cfg,
     band_cfg,
     tracker_cfg,
+    sim_cfg,
     tracks_array,
     LIB_PATH,
 )

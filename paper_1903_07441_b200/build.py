@@ -7,7 +7,7 @@ import sys
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_HERE)
-SOURCES = ["api.cu", "k_relax.cu", "k_stamp.cu", "k_path.cu", "k_track.cu"]
+SOURCES = ["api.cu", "k_relax.cu", "k_stamp.cu", "k_path.cu", "k_track.cu", "k_sim.cu"]
 HEADERS = ["twg_internal.cuh", "twg_kernels.cuh"]
 OUT = os.path.join(_HERE, "libtwg.so")
 

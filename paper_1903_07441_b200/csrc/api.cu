@@ -647,6 +647,7 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
         preload_stamp_kernels();
         preload_path_kernels();
         preload_track_kernels();
+        preload_sim_kernels();
         preloaded = true;
     }
     CK(launch_init_field(c->u[0], c->P, c->sstride, c->W, c->H, c->B, c->stream));
@@ -673,7 +674,9 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
                     c->d_where,  c->d_cur,     c->d_flags, c->d_meta,  c->d_wcfg,   c->d_tracks,   c->d_t,
                     c->d_j,      c->d_pred,    c->d_boxes, c->d_params, c->d_track_off, c->d_cells, c->d_wp,
                     c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
-                    c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det};
+                    c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det,
+                    c->d_sim_rob, c->d_sim_int, c->d_sim_goal, c->d_sim_nobs, c->d_sim_obs, c->d_sim_obs_old,
+                    c->d_sim_speed, c->d_sim_det, c->d_sim_hist};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -900,30 +903,20 @@ TWG_API twg_status twg_get_warp(twg_ctx* c, int32_t b, int32_t n, int32_t* t, in
     return TWG_OK;
 }
 
-TWG_API twg_status twg_track_update(twg_ctx* c, int32_t b, const double* det_xy, const int32_t* n_det,
-                                    const twg_warp_cfg* wc, const twg_tracker_cfg* cfg, int32_t* n_tracks) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (!n_det || !wc || !cfg || b < -1 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    if (!(cfg->sigma_z >= 0.0) || !(cfg->gate >= 0.0) || !(cfg->spawn_var_pos >= 0.0) || !(cfg->spawn_var_vel >= 0.0) ||
-        cfg->prune_after < 0 || cfg->max_tracks < 0)
-        return fail(c, TWG_E_INVALID_ARG, "tracker cfg: sigma_z, gate, variances >= 0, prune_after, max_tracks >= 0");
-    const int nreq = b < 0 ? c->B : 1;
-    std::vector<TrkReq> rq(nreq);
-    int64_t total = 0;
+namespace {
+// Row f1 tick for the requests rq (det_off relative to `det`, a device array of (x, y) pairs).
+twg_status track_core(twg_ctx* c, std::vector<TrkReq> rq, const double2* det, const twg_warp_cfg* wc,
+                      const twg_tracker_cfg* cfg, std::vector<int>& n_out) {
+    twg_status st = TWG_OK;
+    const int nreq = (int)rq.size();
+    n_out.clear();
+    if (nreq == 0) return TWG_OK;
     int max_n = 0, max_m = 0, need_cap = 1;
-    for (int k = 0; k < nreq; ++k) {
-        if (n_det[k] < 0) return fail(c, TWG_E_INVALID_ARG, "negative detection count");
-        rq[k].b = b < 0 ? k : b;
-        rq[k].n = c->scen[rq[k].b].trk_n;
-        rq[k].m = n_det[k];
-        rq[k].det_off = total;
-        total += n_det[k];
-        max_n = std::max(max_n, rq[k].n);
-        max_m = std::max(max_m, rq[k].m);
-        need_cap = std::max(need_cap, rq[k].n + rq[k].m);
+    for (const TrkReq& r : rq) {
+        max_n = std::max(max_n, r.n);
+        max_m = std::max(max_m, r.m);
+        need_cap = std::max(need_cap, r.n + r.m);
     }
-    if (total > 0 && !det_xy) return fail(c, TWG_E_INVALID_ARG, "null detections");
     st = ensure_track_cap(c, need_cap);
     if (st != TWG_OK) return st;
     for (int k = 0; k < nreq; ++k)
@@ -969,31 +962,6 @@ TWG_API twg_status twg_track_update(twg_ctx* c, int32_t b, const double* det_xy,
     };
     st = alloc_req_scratch(pcap);
     if (st != TWG_OK) return st;
-    // detections -> device (double2)
-    const double2* det = nullptr;
-    if (total > 0) {
-        if (is_device_ptr(det_xy) && (reinterpret_cast<uintptr_t>(det_xy) & 15) == 0) {
-            det = reinterpret_cast<const double2*>(det_xy);
-        } else {
-            if (c->trk_det_cap < total) {
-                if (c->d_trk_det) cudaFree(c->d_trk_det);
-                c->d_trk_det = nullptr;
-                TWG_CUDA(c, dev_alloc(&c->d_trk_det, (size_t)total));
-                c->trk_det_cap = total;
-            }
-            if (is_device_ptr(det_xy)) {
-                TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_det, det_xy, (size_t)total * sizeof(double2),
-                                            cudaMemcpyDeviceToDevice, c->stream));
-            } else {
-                void* hd = nullptr;
-                TWG_CUDA(c, stage_alloc(c, (size_t)total * sizeof(double2), &hd));
-                std::memcpy(hd, det_xy, (size_t)total * sizeof(double2));
-                TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_det, hd, (size_t)total * sizeof(double2), cudaMemcpyHostToDevice,
-                                            c->stream));
-            }
-            det = c->d_trk_det;
-        }
-    }
     TrackArgs t;
     t.trk = c->d_tracks;
     t.missed = c->d_missed;
@@ -1067,9 +1035,64 @@ TWG_API twg_status twg_track_update(twg_ctx* c, int32_t b, const double* det_xy,
         todo.swap(again);
         todo_idx.swap(again_idx);
     }
-    if (n_tracks)
-        for (int k = 0; k < nreq; ++k) n_tracks[k] = result_n[k];
+    n_out.assign(result_n.begin(), result_n.end());
     return (twg_status)worst;
+}
+
+
+}  // namespace
+
+TWG_API twg_status twg_track_update(twg_ctx* c, int32_t b, const double* det_xy, const int32_t* n_det,
+                                    const twg_warp_cfg* wc, const twg_tracker_cfg* cfg, int32_t* n_tracks) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!n_det || !wc || !cfg || b < -1 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    if (!(cfg->sigma_z >= 0.0) || !(cfg->gate >= 0.0) || !(cfg->spawn_var_pos >= 0.0) || !(cfg->spawn_var_vel >= 0.0) ||
+        cfg->prune_after < 0 || cfg->max_tracks < 0)
+        return fail(c, TWG_E_INVALID_ARG, "tracker cfg: sigma_z, gate, variances >= 0, prune_after, max_tracks >= 0");
+    const int nreq = b < 0 ? c->B : 1;
+    std::vector<TrkReq> rq(nreq);
+    int64_t total = 0;
+    for (int k = 0; k < nreq; ++k) {
+        if (n_det[k] < 0) return fail(c, TWG_E_INVALID_ARG, "negative detection count");
+        rq[k].b = b < 0 ? k : b;
+        rq[k].n = c->scen[rq[k].b].trk_n;
+        rq[k].m = n_det[k];
+        rq[k].det_off = total;
+        total += n_det[k];
+    }
+    if (total > 0 && !det_xy) return fail(c, TWG_E_INVALID_ARG, "null detections");
+    // detections -> device (double2)
+    const double2* det = nullptr;
+    if (total > 0) {
+        if (is_device_ptr(det_xy) && (reinterpret_cast<uintptr_t>(det_xy) & 15) == 0) {
+            det = reinterpret_cast<const double2*>(det_xy);
+        } else {
+            if (c->trk_det_cap < total) {
+                if (c->d_trk_det) cudaFree(c->d_trk_det);
+                c->d_trk_det = nullptr;
+                TWG_CUDA(c, dev_alloc(&c->d_trk_det, (size_t)total));
+                c->trk_det_cap = total;
+            }
+            if (is_device_ptr(det_xy)) {
+                TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_det, det_xy, (size_t)total * sizeof(double2),
+                                            cudaMemcpyDeviceToDevice, c->stream));
+            } else {
+                void* hd = nullptr;
+                TWG_CUDA(c, stage_alloc(c, (size_t)total * sizeof(double2), &hd));
+                std::memcpy(hd, det_xy, (size_t)total * sizeof(double2));
+                TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_det, hd, (size_t)total * sizeof(double2), cudaMemcpyHostToDevice,
+                                            c->stream));
+            }
+            det = c->d_trk_det;
+        }
+    }
+    std::vector<int> nout;
+    st = track_core(c, rq, det, wc, cfg, nout);
+    if (st < 0) return st;
+    if (n_tracks)
+        for (int k = 0; k < nreq; ++k) n_tracks[k] = nout[k];
+    return st;
 }
 
 TWG_API twg_status twg_get_tracks(twg_ctx* c, int32_t b, twg_track* out, int32_t* missed, int32_t cap, int32_t* n) {
@@ -1086,6 +1109,259 @@ TWG_API twg_status twg_get_tracks(twg_ctx* c, int32_t b, twg_track* out, int32_t
         if (missed)
             TWG_CUDA(c, cudaMemcpyAsync(missed, c->d_missed + o, k * sizeof(int), cudaMemcpyDefault, c->stream));
     }
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TWG_OK;
+}
+
+namespace {
+// Simulator buffers with room for `ocap` obstacles per trial (contents kept when growing).
+twg_status ensure_sim(twg_ctx* c, int ocap) {
+    const size_t B = c->B;
+    if (!c->d_sim_rob) {
+        TWG_CUDA(c, dev_alloc(&c->d_sim_rob, B * 6));
+        TWG_CUDA(c, dev_alloc(&c->d_sim_int, B * 2));
+        TWG_CUDA(c, dev_alloc(&c->d_sim_goal, B * 2));
+        TWG_CUDA(c, dev_alloc(&c->d_sim_nobs, B));
+        TWG_CUDA(c, dev_alloc(&c->d_sim_hist, B * 36));
+        c->sim_rob.assign(B * 6, 0.0);
+        c->sim_ticks.assign(B, 0);
+        c->sim_status.assign(B, 4);
+        c->sim_nobs.assign(B, 0);
+        std::vector<int> init(2 * B, 0);
+        for (size_t b = 0; b < B; ++b) init[B + b] = 4;  // idle
+        TWG_CUDA(c, cudaMemcpy(c->d_sim_int, init.data(), 2 * B * sizeof(int), cudaMemcpyHostToDevice));
+        TWG_CUDA(c, cudaMemset(c->d_sim_nobs, 0, B * sizeof(int)));
+    }
+    if (ocap <= c->sim_ocap) return TWG_OK;
+    const int nc = std::max(ocap, std::max(2 * c->sim_ocap, 16));
+    double *o, *oo, *sp;
+    double2* dt;
+    TWG_CUDA(c, dev_alloc(&o, B * nc * 4));
+    TWG_CUDA(c, dev_alloc(&oo, B * nc * 4));
+    TWG_CUDA(c, dev_alloc(&sp, B * nc));
+    TWG_CUDA(c, dev_alloc(&dt, B * nc));
+    if (c->sim_ocap > 0) {
+        const int oc = c->sim_ocap;
+        TWG_CUDA(c, cudaMemcpy2DAsync(o, nc * 4 * sizeof(double), c->d_sim_obs, oc * 4 * sizeof(double),
+                                      oc * 4 * sizeof(double), B, cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaMemcpy2DAsync(sp, nc * sizeof(double), c->d_sim_speed, oc * sizeof(double), oc * sizeof(double),
+                                      B, cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaMemcpy2DAsync(dt, nc * sizeof(double2), c->d_sim_det, oc * sizeof(double2),
+                                      oc * sizeof(double2), B, cudaMemcpyDeviceToDevice, c->stream));
+        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+        cudaFree(c->d_sim_obs);
+        cudaFree(c->d_sim_obs_old);
+        cudaFree(c->d_sim_speed);
+        cudaFree(c->d_sim_det);
+    }
+    c->d_sim_obs = o;
+    c->d_sim_obs_old = oo;
+    c->d_sim_speed = sp;
+    c->d_sim_det = dt;
+    c->sim_ocap = nc;
+    return TWG_OK;
+}
+
+bool sim_cfg_ok(const twg_sim_cfg* f) {
+    return f && f->dt > 0.0 && f->robot_radius >= 0.0 && f->obstacle_radius >= 0.0 && f->goal_radius >= 0.0 &&
+           f->turn_distance >= 0.0 && f->heading_sigma >= 0.0 && f->det_sigma >= 0.0 && f->turn_max >= 0.0 &&
+           f->max_ticks > 0 && f->init_max_sweeps >= 0;
+}
+
+SimArgs sim_args(twg_ctx* c, const twg_sim_cfg* f) {
+    SimArgs a;
+    a.B = c->B;
+    a.W = c->W;
+    a.H = c->H;
+    a.ocap = c->sim_ocap;
+    a.cs = c->cs;
+    a.ox = c->ox;
+    a.oy = c->oy;
+    a.mask = c->mask;
+    a.rob = c->d_sim_rob;
+    a.ticks = c->d_sim_int;
+    a.status = c->d_sim_int + c->B;
+    a.goal = c->d_sim_goal;
+    a.n_obs = c->d_sim_nobs;
+    a.obs = c->d_sim_obs;
+    a.obs_old = c->d_sim_obs_old;
+    a.obs_speed = c->d_sim_speed;
+    a.det = c->d_sim_det;
+    a.hist = c->d_sim_hist;
+    a.meta = c->d_meta;
+    a.dt = f->dt;
+    a.r_robot = f->robot_radius;
+    a.r_obs = f->obstacle_radius;
+    a.goal_r = f->goal_radius;
+    a.turn_dist = f->turn_distance;
+    a.sigma_h = f->heading_sigma;
+    a.sigma_z = f->det_sigma;
+    a.cos_d = std::cos(f->turn_max);  // host libm (C25)
+    a.sin_d = std::sin(f->turn_max);
+    for (int k = 0; k < 37; ++k) a.cos_bins[k] = std::cos(k * 5.0 * M_PI / 180.0);
+    a.seed = f->seed;
+    a.max_ticks = f->max_ticks;
+    return a;
+}
+}  // namespace
+
+TWG_API twg_status twg_sim_reset(twg_ctx* c, int32_t b, const twg_robot* robot, int32_t goal_x, int32_t goal_y,
+                                 const double* obstacles, int32_t n, const twg_sim_cfg* cfg) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!robot || b < 0 || b >= c->B || n < 0 || (n > 0 && !obstacles) || !sim_cfg_ok(cfg))
+        return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    if (c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "the simulator is not available on a row slab");
+    st = ensure_sim(c, std::max(n, 1));
+    if (st != TWG_OK) return st;
+    // Alg. 1 "Initialize the 2D map and harmonic potential values" (C36): static map + goal,
+    // no tracks, cold, relaxed to init_tol (checked every 100 sweeps)
+    EncodeReq r{b, *robot, goal_x, goal_y, 0, 0};
+    c->scen[b].encoded = false;
+    twg_warp_cfg wz;  // no tracks: the warp configuration is not used
+    std::memset(&wz, 0, sizeof(wz));
+    st = encode(c, {r}, nullptr, &wz, 0);
+    if (st < 0) return st;
+    std::vector<int> part(c->B, 0);
+    part[b] = 1;
+    twg_relax_cfg rc;
+    std::memset(&rc, 0, sizeof(rc));
+    rc.max_sweeps = cfg->init_max_sweeps;
+    rc.check_every = 100;
+    rc.tol = cfg->init_tol;
+    st = relax(c, &rc, part, nullptr, nullptr);
+    if (st != TWG_OK) return st;
+    // trial state
+    const int oc = c->sim_ocap;
+    char* h = nullptr;
+    const size_t bytes = 6 * sizeof(double) + 2 * sizeof(double) + (size_t)oc * 5 * sizeof(double);
+    TWG_CUDA(c, stage_alloc(c, bytes, reinterpret_cast<void**>(&h)));
+    double* hr = reinterpret_cast<double*>(h);
+    hr[0] = robot->x;
+    hr[1] = robot->y;
+    hr[2] = std::cos(robot->theta);  // host libm (C25)
+    hr[3] = std::sin(robot->theta);
+    hr[4] = robot->speed;
+    hr[5] = 0.0;
+    double* hg = hr + 6;
+    hg[0] = c->ox + ((double)goal_x + 0.5) * c->cs;
+    hg[1] = c->oy + ((double)goal_y + 0.5) * c->cs;
+    double* ho = hg + 2;
+    double* hs = ho + (size_t)oc * 4;
+    std::memset(ho, 0, (size_t)oc * 5 * sizeof(double));
+    for (int i = 0; i < n; ++i) {
+        for (int q = 0; q < 4; ++q) ho[4 * i + q] = obstacles[4 * i + q];
+        hs[i] = std::sqrt(obstacles[4 * i + 2] * obstacles[4 * i + 2] + obstacles[4 * i + 3] * obstacles[4 * i + 3]);
+    }
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_rob + 6 * b, hr, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_goal + 2 * b, hg, 2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_obs + (size_t)b * oc * 4, ho, (size_t)oc * 4 * sizeof(double),
+                                cudaMemcpyHostToDevice, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_speed + (size_t)b * oc, hs, (size_t)oc * sizeof(double),
+                                cudaMemcpyHostToDevice, c->stream));
+    TWG_CUDA(c, cudaMemsetAsync(c->d_sim_int + b, 0, sizeof(int), c->stream));          // ticks
+    TWG_CUDA(c, cudaMemsetAsync(c->d_sim_int + c->B + b, 0, sizeof(int), c->stream));   // running
+    TWG_CUDA(c, cudaMemsetAsync(c->d_sim_hist + 36 * b, 0, 36 * sizeof(int), c->stream));
+    int* hn = nullptr;
+    TWG_CUDA(c, stage_alloc(c, sizeof(int), reinterpret_cast<void**>(&hn)));
+    *hn = n;
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_nobs + b, hn, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    SimArgs a = sim_args(c, cfg);
+    TWG_CUDA(c, launch_sim_sense(a, b, c->stream));
+    c->launches += 1;
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int q = 0; q < 6; ++q) c->sim_rob[6 * b + q] = hr[q];
+    c->sim_ticks[b] = 0;
+    c->sim_status[b] = 0;
+    c->sim_nobs[b] = n;
+    c->scen[b].trk_n = 0;
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_sim_tick(twg_ctx* c, const twg_sim_cfg* cfg, const twg_warp_cfg* warp,
+                                const twg_relax_cfg* rcfg, const twg_band_cfg* bcfg, const twg_tracker_cfg* tcfg,
+                                twg_sim_trial* out, int32_t* running) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!sim_cfg_ok(cfg) || !warp || !rcfg || !bcfg || !tcfg) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    if (!c->d_sim_rob) return fail(c, TWG_E_INVALID_ARG, "twg_sim_tick before twg_sim_reset");
+    std::vector<int> act;
+    for (int b = 0; b < c->B; ++b)
+        if (c->sim_status[b] == 0) act.push_back(b);
+    int worst = 0;
+    if (!act.empty()) {
+        // f1: tracker tick on this tick's detections
+        std::vector<TrkReq> rq(act.size());
+        for (size_t k = 0; k < act.size(); ++k) {
+            const int b = act[k];
+            rq[k].b = b;
+            rq[k].n = c->scen[b].trk_n;
+            rq[k].m = c->sim_nobs[b];
+            rq[k].det_off = (int64_t)b * c->sim_ocap;
+        }
+        std::vector<int> nout;
+        st = track_core(c, rq, c->d_sim_det, warp, tcfg, nout);
+        if (st < 0) return st;
+        worst = std::max(worst, (int)st);
+        // a1-a9 from the resident tracks
+        std::vector<EncodeReq> reqs;
+        for (int b : act) {
+            twg_robot rb;
+            rb.x = c->sim_rob[6 * b];
+            rb.y = c->sim_rob[6 * b + 1];
+            rb.theta = std::atan2(c->sim_rob[6 * b + 3], c->sim_rob[6 * b + 2]);  // host libm (C25)
+            rb.speed = c->sim_rob[6 * b + 4];
+            reqs.push_back(EncodeReq{b, rb, c->scen[b].gx, c->scen[b].gy, c->scen[b].trk_n, 0});
+        }
+        st = encode(c, reqs, nullptr, warp, rcfg->warm_start, true);
+        if (st < 0) return st;
+        std::vector<int> part(c->B, 0);
+        for (int b : act) part[b] = 1;
+        st = relax(c, rcfg, part, nullptr, nullptr);
+        if (st != TWG_OK) return st;
+        st = path(c, act, bcfg);
+        if (st != TWG_OK) return st;
+        // simulator step + next detections
+        SimArgs a = sim_args(c, cfg);
+        TWG_CUDA(c, launch_sim_move(a, c->stream));
+        TWG_CUDA(c, launch_sim_sense(a, -1, c->stream));
+        c->launches += 2;
+    }
+    // read back the trial states
+    const size_t B = c->B;
+    char* h = nullptr;
+    TWG_CUDA(c, stage_alloc(c, B * 6 * sizeof(double) + 2 * B * sizeof(int), reinterpret_cast<void**>(&h)));
+    double* hr = reinterpret_cast<double*>(h);
+    int* hi = reinterpret_cast<int*>(hr + 6 * B);
+    TWG_CUDA(c, cudaMemcpyAsync(hr, c->d_sim_rob, B * 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(hi, c->d_sim_int, 2 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    int nrun = 0;
+    for (size_t b = 0; b < B; ++b) {
+        for (int q = 0; q < 6; ++q) c->sim_rob[6 * b + q] = hr[6 * b + q];
+        c->sim_ticks[b] = hi[b];
+        c->sim_status[b] = hi[B + b];
+        nrun += c->sim_status[b] == 0;
+        if (out) {
+            out[b].x = hr[6 * b];
+            out[b].y = hr[6 * b + 1];
+            out[b].hx = hr[6 * b + 2];
+            out[b].hy = hr[6 * b + 3];
+            out[b].speed = hr[6 * b + 4];
+            out[b].length = hr[6 * b + 5];
+            out[b].ticks = hi[b];
+            out[b].status = hi[B + b];
+        }
+    }
+    if (running) *running = nrun;
+    return (twg_status)worst;
+}
+
+TWG_API twg_status twg_sim_histogram(twg_ctx* c, int32_t b, int32_t* hist) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!hist || b < 0 || b >= c->B || !c->d_sim_hist) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    TWG_CUDA(c, cudaMemcpyAsync(hist, c->d_sim_hist + 36 * b, 36 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     TWG_CUDA(c, cudaStreamSynchronize(c->stream));
     return TWG_OK;
 }

@@ -180,6 +180,19 @@ struct twg_ctx {
     twg::TrkReq* d_trk_req = nullptr;
     double2* d_trk_det = nullptr;
     int64_t trk_det_cap = 0;
+    // closed-loop simulator (row f2)
+    int sim_ocap = 0;
+    double* d_sim_rob = nullptr;       // [B][6]
+    int* d_sim_int = nullptr;          // [2][B]: ticks, status
+    double* d_sim_goal = nullptr;      // [B][2]
+    int* d_sim_nobs = nullptr;         // [B]
+    double* d_sim_obs = nullptr;       // [B][ocap][4]
+    double* d_sim_obs_old = nullptr;   // [B][ocap][4]
+    double* d_sim_speed = nullptr;     // [B][ocap]
+    double2* d_sim_det = nullptr;      // [B][ocap]
+    int* d_sim_hist = nullptr;         // [B][36]
+    std::vector<double> sim_rob;       // host mirror [B][6]
+    std::vector<int> sim_ticks, sim_status, sim_nobs;
     twg::ScenParams* d_params = nullptr;
     int params_cap = 0;
     twg::WarpCfgDev* d_wcfg = nullptr;

@@ -89,10 +89,35 @@ struct PathArgs {
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
 cudaError_t launch_index_dir(const PathArgs& p, cudaStream_t st);  // k_index_dir alone (twg_index_matrix)
 
+// k_sim.cu (row f2: closed-loop simulator)
+struct SimArgs {
+    int B, W, H, ocap;
+    double cs, ox, oy;
+    const uint8_t* mask;     // [B][H][W]
+    double* rob;             // [B][6]: x, y, hx, hy, speed, length
+    int* ticks;              // [B]
+    int* status;             // [B]: 0 running, 1 success, 2 collision, 3 timeout, 4 idle
+    const double* goal;      // [B][2] goal centre (m)
+    const int* n_obs;        // [B]
+    double* obs;             // [B][ocap][4]: x, y, vx, vy
+    double* obs_old;         // [B][ocap][4] scratch
+    const double* obs_speed; // [B][ocap]
+    double2* det;            // [B][ocap] detections of the current tick
+    int* hist;               // [B][36] turning-angle histogram (5 degree bins)
+    const PathMeta* meta;    // [B] this tick's plan (walk status, next waypoint)
+    double dt, r_robot, r_obs, goal_r, turn_dist, sigma_h, sigma_z, cos_d, sin_d;
+    double cos_bins[37];
+    uint64_t seed;
+    int max_ticks;
+};
+cudaError_t launch_sim_move(const SimArgs& a, cudaStream_t st);
+cudaError_t launch_sim_sense(const SimArgs& a, int only, cudaStream_t st);
+
 // Module preloading (called once by twg_create)
 void preload_relax_kernels();
 void preload_stamp_kernels();
 void preload_path_kernels();
 void preload_track_kernels();
+void preload_sim_kernels();
 
 }  // namespace twg

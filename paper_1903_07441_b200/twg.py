@@ -59,6 +59,19 @@ class TrackerCfg(C.Structure):
                 ("spawn_var_vel", C.c_double), ("prune_after", C.c_int32), ("max_tracks", C.c_int32)]
 
 
+class SimCfg(C.Structure):
+    _fields_ = [("dt", C.c_double), ("robot_radius", C.c_double), ("obstacle_radius", C.c_double),
+                ("goal_radius", C.c_double), ("turn_distance", C.c_double), ("heading_sigma", C.c_double),
+                ("det_sigma", C.c_double), ("turn_max", C.c_double), ("seed", C.c_uint64),
+                ("max_ticks", C.c_int32), ("init_max_sweeps", C.c_int32), ("init_tol", C.c_float),
+                ("reserved", C.c_int32)]
+
+
+class SimTrial(C.Structure):
+    _fields_ = [("x", C.c_double), ("y", C.c_double), ("hx", C.c_double), ("hy", C.c_double),
+                ("speed", C.c_double), ("length", C.c_double), ("ticks", C.c_int32), ("status", C.c_int32)]
+
+
 class PlanResult(C.Structure):
     _fields_ = [("status", C.c_int32), ("sweeps", C.c_int32), ("n_cells", C.c_int32), ("n_smooth", C.c_int32),
                 ("residual", C.c_float), ("next_x", C.c_float), ("next_y", C.c_float), ("walk_status", C.c_int32)]
@@ -81,6 +94,11 @@ SIGNATURES = [
     ("twg_get_warp", C.c_int32, [_P, C.c_int32, C.c_int32, _P, _P, _P]),
     ("twg_track_update", C.c_int32, [_P, C.c_int32, _P, _P, C.POINTER(WarpCfg), C.POINTER(TrackerCfg), _P]),
     ("twg_get_tracks", C.c_int32, [_P, C.c_int32, _P, _P, C.c_int32, C.POINTER(C.c_int32)]),
+    ("twg_sim_reset", C.c_int32, [_P, C.c_int32, C.POINTER(Robot), C.c_int32, C.c_int32, _P, C.c_int32,
+                                  C.POINTER(SimCfg)]),
+    ("twg_sim_tick", C.c_int32, [_P, C.POINTER(SimCfg), C.POINTER(WarpCfg), C.POINTER(RelaxCfg), C.POINTER(BandCfg),
+                                 C.POINTER(TrackerCfg), _P, C.POINTER(C.c_int32)]),
+    ("twg_sim_histogram", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_index_matrix", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_warp_map", C.c_int32, [_P, C.POINTER(Robot), C.c_double, _P]),
     ("twg_field_ptr", C.c_int32, [_P, C.c_int32, C.POINTER(_P), C.POINTER(C.c_int64)]),
@@ -157,6 +175,13 @@ def relax_cfg(max_sweeps=100, check_every=0, warm_start=1, temporal_depth=0, tol
 
 def tracker_cfg(sigma_z=0.05, gate=0.5, spawn_var_pos=0.25, spawn_var_vel=1.0, prune_after=10, max_tracks=0):
     return TrackerCfg(sigma_z, gate, spawn_var_pos, spawn_var_vel, prune_after, max_tracks)
+
+
+def sim_cfg(dt=0.1, robot_radius=0.25, obstacle_radius=0.25, goal_radius=0.3, turn_distance=0.5, heading_sigma=0.02,
+            det_sigma=0.05, turn_max=0.15707963267948966, seed=1, max_ticks=1000, init_max_sweeps=1_000_000,
+            init_tol=1e-6):
+    return SimCfg(dt, robot_radius, obstacle_radius, goal_radius, turn_distance, heading_sigma, det_sigma, turn_max,
+                  seed, max_ticks, init_max_sweeps, init_tol, 0)
 
 
 def band_cfg(iterations=50, max_len=4096, max_smooth=8192, step=0.25, k_t=1.0):
@@ -286,6 +311,28 @@ class Planner:
         mis = np.zeros(max(n.value, 1), np.int32)
         _check(self.ctx, lib().twg_get_tracks(self.ctx, b, _ptr(out), _ptr(mis), n.value, C.byref(n)))
         return out[: n.value], mis[: n.value]
+
+    # -- f2 closed-loop simulator
+    def sim_reset(self, b, robot, goal, obstacles, cfg):
+        """twg_sim_reset: obstacles [n, 4] (x, y, vx, vy) true states."""
+        o = np.ascontiguousarray(np.asarray(obstacles, np.float64).reshape(-1, 4))
+        r = Robot(*[float(v) for v in robot])
+        return _check(self.ctx, lib().twg_sim_reset(self.ctx, b, C.byref(r), int(goal[0]), int(goal[1]),
+                                                    _ptr(o) if len(o) else None, len(o), C.byref(cfg)))
+
+    def sim_tick(self, cfg, wcfg, rcfg, bcfg, tcfg):
+        """twg_sim_tick: returns (status, [SimTrial] * batch, running)."""
+        out = (SimTrial * self.B)()
+        run = C.c_int32()
+        st = lib().twg_sim_tick(self.ctx, C.byref(cfg), C.byref(wcfg), C.byref(rcfg), C.byref(bcfg), C.byref(tcfg),
+                                out, C.byref(run))
+        _check(self.ctx, st, ok=(OK, W_GOAL_SWALLOWED, W_TRUNCATED, W_SINGULAR_INNOVATION))
+        return st, list(out), run.value
+
+    def sim_histogram(self, b=0):
+        h = np.zeros(36, np.int32)
+        _check(self.ctx, lib().twg_sim_histogram(self.ctx, b, _ptr(h)))
+        return h
 
     def index_matrix(self, b=0, out=None):
         """twg_index_matrix: uint8 [H, W] M_idx of scenario b (0..3 move, 4 goal, 5 obstacle, 6 none)."""

@@ -19,6 +19,8 @@ from .gen import (  # noqa: F401
     scene_c5,
     advance_scene,
     detections,
+    SimCfg,
+    scene_sim,
     annulus_fixed,
     random_small_map,
     CONFIGS,

@@ -236,6 +236,41 @@ def detections(scene: Scene, tick: int, sigma_z: float = 0.05, p_miss: float = 0
     return np.ascontiguousarray(z)
 
 
+@dataclass
+class SimCfg:
+    """Closed-loop simulator configuration (row f2; C31-C35).  Plain inputs."""
+    dt: float = 0.1
+    robot_radius: float = 0.25
+    obstacle_radius: float = 0.25
+    goal_radius: float = 0.3
+    turn_distance: float = 0.5
+    heading_sigma: float = 0.02
+    det_sigma: float = 0.05
+    turn_max: float = 0.15707963267948966  # 9 degrees per tick = 90 deg/s (S:448)
+    seed: int = 1
+    max_ticks: int = 1000
+    init_tol: float = 1e-6       # Alg. 1 "Initialize ... harmonic potential values" (P:676): relax the
+    init_max_sweeps: int = 1_000_000  # tick-0 static field to this residual (checked every 100 sweeps)
+
+
+def scene_sim(seed: int, n_obs: int, N: int = 256, n_seg: int = 6, cs: float = 0.1) -> Scene:
+    """A 25.6 m x 25.6 m map with `n_seg` wall segments, the robot near one corner heading
+    to a goal near the opposite one, and `n_obs` robot-sized obstacles wandering at 0.2-0.5 m/s
+    (Table 1 uses 1, 2, 4, 8, 12, 16).  truth = obstacle states (x, y, vx, vy); no tracks (the
+    tracker spawns them from detections)."""
+    rng = np.random.default_rng([seed, 1903])
+    W = H = N
+    static = _walls(rng, W, H, cs, n_seg, lmin=2.0, lmax=8.0)
+    rx, ry = 1.55, 1.55
+    gx, gy = N - 16, N - 16
+    _clear_disk(static, rx / cs, ry / cs, 1.5 / cs)
+    _clear_disk(static, gx + 0.5, gy + 0.5, 1.5 / cs)
+    theta = math.atan2((gy + 0.5) * cs - ry, (gx + 0.5) * cs - rx)
+    truth, _ = _tracks(rng, n_obs, W, H, cs, static, (rx, ry), ((gx + 0.5) * cs, (gy + 0.5) * cs))
+    return Scene(f"sim_s{seed}_n{n_obs}", W, H, cs, (0.0, 0.0), static, (rx, ry, theta, 0.4), (gx, gy),
+                 np.zeros((0, 20)), default_warp_cfg(), seed, truth)
+
+
 def random_small_map(seed: int, N: int = 48, n_disks=(3, 11), n_walls=(0, 4)):
     """Random N x N static map with disks and walls plus a goal cell and a start cell.
 
