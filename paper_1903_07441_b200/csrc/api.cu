@@ -161,12 +161,20 @@ twg_status ensure_track_cap(twg_ctx* c, int cap) {
     return TWG_OK;
 }
 
+// Parameter block: [WarpCfgDev | pad to 256 B | ScenParams x n], so one copy uploads both.
+constexpr size_t kParamOff = 256;
+static_assert(sizeof(WarpCfgDev) <= kParamOff, "warp cfg does not fit the parameter block header");
 twg_status ensure_params(twg_ctx* c, int n) {
-    if (n <= c->params_cap) return TWG_OK;
-    if (c->d_params) cudaFree(c->d_params);
+    if (n <= c->params_cap && c->d_param_block) return TWG_OK;
+    if (c->d_param_block) cudaFree(c->d_param_block);
+    c->d_param_block = nullptr;
     c->d_params = nullptr;
-    TWG_CUDA(c, dev_alloc(&c->d_params, n));
-    c->params_cap = n;
+    c->d_wcfg = nullptr;
+    const int nc = std::max(n, 1);
+    TWG_CUDA(c, dev_alloc(&c->d_param_block, kParamOff + (size_t)nc * sizeof(ScenParams)));
+    c->d_wcfg = reinterpret_cast<WarpCfgDev*>(c->d_param_block);
+    c->d_params = reinterpret_cast<ScenParams*>(c->d_param_block + kParamOff);
+    c->params_cap = nc;
     return TWG_OK;
 }
 
@@ -320,17 +328,14 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     w.hmax = wc->horizon_max;
     w.hmode = wc->horizon_mode;
     w.fmode = wc->footprint_mode;
-    const size_t pbytes = ns * sizeof(ScenParams);
+    // warp cfg + per-scenario params: one copy into the parameter block (warning flags are cleared
+    // by k_goal_reset, which runs before the stamping kernels that set them)
+    const size_t pbytes = kParamOff + ns * sizeof(ScenParams);
     char* hs = nullptr;
-    TWG_CUDA(c, stage_alloc(c, pbytes + sizeof(WarpCfgDev) + 64, reinterpret_cast<void**>(&hs)));
-    std::memcpy(hs, ps.data(), pbytes);
-    std::memcpy(hs + pbytes, &w, sizeof(w));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_params, hs, pbytes, cudaMemcpyHostToDevice, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_wcfg, hs + pbytes, sizeof(w), cudaMemcpyHostToDevice, c->stream));
-    // clear warning flags of these scenarios (one memset when the call covers every scenario)
-    if (ns == c->B) TWG_CUDA(c, cudaMemsetAsync(c->d_flags, 0, c->B * sizeof(int), c->stream));
-    else
-        for (int k = 0; k < ns; ++k) TWG_CUDA(c, cudaMemsetAsync(c->d_flags + reqs[k].b, 0, sizeof(int), c->stream));
+    TWG_CUDA(c, stage_alloc(c, pbytes, reinterpret_cast<void**>(&hs)));
+    std::memcpy(hs, &w, sizeof(w));
+    std::memcpy(hs + kParamOff, ps.data(), ns * sizeof(ScenParams));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_param_block, hs, pbytes, cudaMemcpyHostToDevice, c->stream));
     EncodeArgs e;
     e.u0 = c->u[0];
     e.u1 = c->u[1];
@@ -415,19 +420,19 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
     const float tol = cfg->tol;
     int check = (tol > 0.0f && cfg->check_every > 0) ? cfg->check_every : std::max(maxs, 1);
     const int sync_every = cfg->sync_every > 0 ? cfg->sync_every : 64;
-    // control arrays: done = !participating; sweeps = 0; residual bits = 0; cur uploaded
+    // control arrays [done | cur | sweeps | where | res bits | res]: one copy (done = !participating,
+    // where = -1: not (yet) finished)
     int* hs = nullptr;
-    TWG_CUDA(c, stage_alloc(c, 2 * B * sizeof(int), reinterpret_cast<void**>(&hs)));
+    TWG_CUDA(c, stage_alloc(c, 6 * B * sizeof(int), reinterpret_cast<void**>(&hs)));
     for (int b = 0; b < B; ++b) {
         hs[b] = part[b] ? 0 : 1;
         hs[B + b] = c->cur[b];
+        hs[2 * B + b] = 0;
+        hs[3 * B + b] = -1;
+        hs[4 * B + b] = 0;
+        hs[5 * B + b] = 0;  // +0.0f
     }
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_done, hs, B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_cur, hs + B, B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    TWG_CUDA(c, cudaMemsetAsync(c->d_sweeps, 0, B * sizeof(int), c->stream));
-    TWG_CUDA(c, cudaMemsetAsync(c->d_where, 0xff, B * sizeof(int), c->stream));  // -1: not (yet) finished
-    TWG_CUDA(c, cudaMemsetAsync(c->d_res_bits, 0, B * sizeof(unsigned), c->stream));
-    TWG_CUDA(c, cudaMemsetAsync(c->d_res, 0, B * sizeof(float), c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_ctl, hs, 6 * B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     int nscen = 0;
     for (int b = 0; b < B; ++b) nscen += part[b] ? 1 : 0;
 
@@ -512,11 +517,10 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
             if (part[b]) c->cur[b] ^= (lp & 1);
     }
     if (sweeps_done || residual) {
-        int* hsw = nullptr;
-        TWG_CUDA(c, stage_alloc(c, 2 * B * sizeof(int), reinterpret_cast<void**>(&hsw)));
-        float* hr = reinterpret_cast<float*>(hsw + B);
-        TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        TWG_CUDA(c, cudaMemcpyAsync(hr, c->d_res, B * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        int* hsw = nullptr;  // [sweeps | where | res bits | res] in one copy
+        TWG_CUDA(c, stage_alloc(c, 4 * B * sizeof(int), reinterpret_cast<void**>(&hsw)));
+        float* hr = reinterpret_cast<float*>(hsw + 3 * B);
+        TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, 4 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         TWG_CUDA(c, cudaStreamSynchronize(c->stream));
         for (int b = 0; b < B; ++b) {
             if (sweeps_done) sweeps_done[b] = hsw[b];
@@ -628,17 +632,18 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     CK(dev_alloc(&c->u[0], cells));
     CK(dev_alloc(&c->u[1], cells));
     CK(dev_alloc(&c->mask, B * c->H * c->W));
-    CK(dev_alloc(&c->d_done, B));
-    CK(dev_alloc(&c->d_sweeps, B));
-    CK(dev_alloc(&c->d_res_bits, B));
-    CK(dev_alloc(&c->d_res, B));
-    CK(dev_alloc(&c->d_where, B));
-    CK(dev_alloc(&c->d_cur, B));
-    CK(dev_alloc(&c->d_flags, B));
+    CK(dev_alloc(&c->d_ctl, 7 * B));
+    CK(cudaMemset(c->d_ctl, 0, 7 * B * sizeof(int)));
+    c->d_done = c->d_ctl;
+    c->d_cur = c->d_ctl + B;
+    c->d_sweeps = c->d_ctl + 2 * B;
+    c->d_where = c->d_ctl + 3 * B;
+    c->d_res_bits = reinterpret_cast<unsigned*>(c->d_ctl + 4 * B);
+    c->d_res = reinterpret_cast<float*>(c->d_ctl + 5 * B);
+    c->d_flags = c->d_ctl + 6 * B;
     CK(dev_alloc(&c->d_meta, B));
     CK(dev_alloc(&c->d_idx, cells));
     CK(dev_alloc(&c->d_dir, cells));
-    CK(dev_alloc(&c->d_wcfg, 1));
     CK(cudaMemsetAsync(c->mask, 0, B * c->H * c->W, c->stream));
     CK(cudaMemsetAsync(c->d_meta, 0, B * sizeof(PathMeta), c->stream));
     static bool preloaded = false;  // eager module loading (process-wide, once)
@@ -670,9 +675,8 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
     if (!c) return TWG_OK;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_done,  c->d_sweeps, c->d_res_bits, c->d_res,
-                    c->d_where,  c->d_cur,     c->d_flags, c->d_meta,  c->d_wcfg,   c->d_tracks,   c->d_t,
-                    c->d_j,      c->d_pred,    c->d_boxes, c->d_params, c->d_track_off, c->d_cells, c->d_wp,
+    void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_ctl,   c->d_meta,   c->d_tracks,   c->d_t,
+                    c->d_j,      c->d_pred,    c->d_boxes, c->d_param_block, c->d_track_off, c->d_cells, c->d_wp,
                     c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
                     c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det,
                     c->d_sim_rob, c->d_sim_int, c->d_sim_goal, c->d_sim_nobs, c->d_sim_obs, c->d_sim_obs_old,
@@ -798,15 +802,13 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
     const int B = c->B;
     const size_t mb = B * sizeof(PathMeta);
     char* h = nullptr;
-    TWG_CUDA(c, stage_alloc(c, mb + 3 * B * sizeof(int), reinterpret_cast<void**>(&h)));
+    TWG_CUDA(c, stage_alloc(c, mb + 5 * B * sizeof(int), reinterpret_cast<void**>(&h)));
     PathMeta* hm = reinterpret_cast<PathMeta*>(h);
-    int* hsw = reinterpret_cast<int*>(h + mb);
-    float* hr = reinterpret_cast<float*>(hsw + B);
-    int* hf = hsw + 2 * B;
+    int* hsw = reinterpret_cast<int*>(h + mb);  // [sweeps | where | res bits | res | flags] in one copy
+    float* hr = reinterpret_cast<float*>(hsw + 3 * B);
+    int* hf = hsw + 4 * B;
     TWG_CUDA(c, cudaMemcpyAsync(hm, c->d_meta, mb, cudaMemcpyDeviceToHost, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(hr, c->d_res, B * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(hf, c->d_flags, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, 5 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (cells_xy) {
         if (b >= 0)
             TWG_CUDA(c, cudaMemcpyAsync(cells_xy, c->d_cells + (int64_t)b * c->path_len_cap,

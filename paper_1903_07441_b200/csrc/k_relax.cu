@@ -21,6 +21,31 @@
 
 namespace twg {
 
+// Programmatic dependent launch (sm_90+): a kernel of the relaxation chain is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so it is launched while the previous kernel
+// drains.  pdl_wait: before touching anything the previous kernel wrote.  pdl_trigger: once this
+// CTA has issued its last work, so the successor's CTAs are only scheduled when every CTA of this
+// grid is finishing (triggering at the start lets early successor CTAs crowd some SMs and
+// unbalances the launch).  Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // Update the cells of parity q (j = q, q + 2 of the lane's float4) of row `c`
 // from rows `up` (y - 1) and `dn` (y + 1).  Returns the largest |du| of the
 // updated free cells in *dmax when TRACK.
@@ -109,6 +134,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     constexpr int HX = halo_cols(T);
     constexpr int WOUT = out_cols(T);
     constexpr int STAGE_F = NW * kStripW;  // floats per ring stage
+    pdl_wait();
     const int b = blockIdx.y;
     if (a.done != nullptr && a.done[b]) return;  // scenario converged: whole CTA exits
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,6 +196,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
         }
     }
 
+    pdl_trigger();
     if (RESID) {
         const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(st.dmax));
         if (lane == 0 && m != 0u) atomicMax(&a.res[b], m);
@@ -222,6 +249,7 @@ __device__ __forceinline__ float jac_cell(float c, float e, float w, float n, fl
 }
 
 __global__ void __launch_bounds__(kJacWarps * 32) k_jacobi(RelaxArgs a, int resid) {
+    pdl_wait();
     const int b = blockIdx.z;
     if (a.done[b]) return;
     const int lane = threadIdx.x & 31;
@@ -258,6 +286,7 @@ __global__ void __launch_bounds__(kJacWarps * 32) k_jacobi(RelaxArgs a, int resi
         up = c;
         c = dn;
     }
+    pdl_trigger();
     if (resid) {
         const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(dmax));
         if (lane == 0 && m != 0u) atomicMax(&a.res[b], m);
@@ -266,7 +295,8 @@ __global__ void __launch_bounds__(kJacWarps * 32) k_jacobi(RelaxArgs a, int resi
 
 cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st) {
     dim3 grid((unsigned)((a.P + kStripW - 1) / kStripW), (a.H + kJacWarps * kJacRows - 1) / (kJacWarps * kJacRows), B);
-    k_jacobi<<<grid, kJacWarps * 32, 0, st>>>(a, resid ? 1 : 0);
+    cudaError_t e = launch_pdl(k_jacobi, grid, dim3(kJacWarps * 32), 0, st, a, resid ? 1 : 0);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -278,6 +308,8 @@ cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st
 __global__ void k_check(int B, int* __restrict__ done, int* __restrict__ sweeps, unsigned* __restrict__ res_bits,
                         float* __restrict__ res_final, int* __restrict__ where, int chunk, int check_every,
                         int max_sweeps, float tol, const int* __restrict__ cur, int lp) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B || done[b]) return;
     const int s = sweeps[b] + chunk;
@@ -314,7 +346,8 @@ static cudaError_t launch_T(const CUtensorMap& m0, const CUtensorMap& m1, const 
         cudaFuncSetAttribute(k_rb_tblock<T, QOFF, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_rb_tblock<T, QOFF, RESID><<<grid, kWarpsPerCta * 32, smem, st>>>(m0, m1, a);
+    cudaError_t e = launch_pdl(k_rb_tblock<T, QOFF, RESID>, grid, dim3(kWarpsPerCta * 32), smem, st, m0, m1, a);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -372,8 +405,9 @@ cudaError_t launch_rb_simple(float* u, int64_t P, int64_t sstride, int W, int H,
 
 cudaError_t launch_check(int B, int* done, int* sweeps, unsigned* res_bits, float* res_final, int* where, int chunk,
                          int check_every, int max_sweeps, float tol, const int* cur, int lp, cudaStream_t st) {
-    k_check<<<(B + 127) / 128, 128, 0, st>>>(B, done, sweeps, res_bits, res_final, where, chunk, check_every,
-                                             max_sweeps, tol, cur, lp);
+    cudaError_t e = launch_pdl(k_check, dim3((B + 127) / 128), dim3(128), 0, st, B, done, sweeps, res_bits, res_final,
+                               where, chunk, check_every, max_sweeps, tol, cur, lp);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

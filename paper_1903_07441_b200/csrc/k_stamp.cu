@@ -51,6 +51,7 @@ __global__ void k_goal_reset(EncodeArgs e) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= e.nscen) return;
     const ScenParams& sp = e.params[k];
+    e.flags[sp.b] = 0;  // warning flags of this call (set by k_stamp, which runs after)
     if (!sp.warm || sp.old_gx < 0 || sp.old_gy < 0 || sp.old_gy >= e.H) return;
     if (sp.old_gx == sp.gx && sp.old_gy == sp.gy) return;
     const int b = sp.b;

@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/twg.h"
@@ -142,6 +143,7 @@ struct twg_ctx {
     int64_t sstride = 0;  // floats per scenario field
     float* u[2] = {nullptr, nullptr};
     std::vector<int> cur;          // per scenario: which buffer holds the current field
+    int* d_ctl = nullptr;          // one allocation [7][B]: done, cur, sweeps, where, res bits, res, flags
     int* d_cur = nullptr;          // device copy used by the tile kernel
     CUtensorMap tmap[2][kMaxT + 1];  // [buffer][T]: box = 128 x (2T + 2) rows
     uint8_t* mask = nullptr;       // device [B][H][W]
@@ -193,7 +195,8 @@ struct twg_ctx {
     int* d_sim_hist = nullptr;         // [B][36]
     std::vector<double> sim_rob;       // host mirror [B][6]
     std::vector<int> sim_ticks, sim_status, sim_nobs;
-    twg::ScenParams* d_params = nullptr;
+    twg::ScenParams* d_params = nullptr;  // inside the parameter block (after d_wcfg)
+    unsigned char* d_param_block = nullptr;
     int params_cap = 0;
     twg::WarpCfgDev* d_wcfg = nullptr;
     int* d_track_off = nullptr;        // scatter offsets + scenario indices of one encode call
