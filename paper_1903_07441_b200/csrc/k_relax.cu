@@ -21,31 +21,6 @@
 
 namespace twg {
 
-// Programmatic dependent launch (sm_90+): a kernel of the relaxation chain is launched with
-// cudaLaunchAttributeProgrammaticStreamSerialization, so it is launched while the previous kernel
-// drains.  pdl_wait: before touching anything the previous kernel wrote.  pdl_trigger: once this
-// CTA has issued its last work, so the successor's CTAs are only scheduled when every CTA of this
-// grid is finishing (triggering at the start lets early successor CTAs crowd some SMs and
-// unbalances the launch).  Without the launch attribute both instructions are no-ops.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                              Args&&... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
-
 // Update the cells of parity q (j = q, q + 2 of the lane's float4) of row `c`
 // from rows `up` (y - 1) and `dn` (y + 1).  Returns the largest |du| of the
 // updated free cells in *dmax when TRACK.

@@ -20,6 +20,7 @@
 namespace twg {
 
 __global__ void k_encode_cold(EncodeArgs e) {
+    pdl_enter();
     const ScenParams& sp = e.params[blockIdx.z];
     if (sp.warm) return;
     const int b = sp.b;
@@ -32,6 +33,7 @@ __global__ void k_encode_cold(EncodeArgs e) {
 }
 
 __global__ void k_unstamp(EncodeArgs e) {
+    pdl_enter();
     const ScenParams& sp = e.params[blockIdx.y];
     if (!sp.warm || (int)blockIdx.x >= sp.n_prev_boxes) return;
     const int b = sp.b;
@@ -48,6 +50,7 @@ __global__ void k_unstamp(EncodeArgs e) {
 }
 
 __global__ void k_goal_reset(EncodeArgs e) {
+    pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= e.nscen) return;
     const ScenParams& sp = e.params[k];
@@ -67,6 +70,7 @@ __device__ __forceinline__ long long round_half_away(double x) {
 }
 
 __global__ void k_track_predict(EncodeArgs e) {
+    pdl_enter();
     const ScenParams& sp = e.params[blockIdx.y];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sp.n_tracks) return;
@@ -166,6 +170,7 @@ __global__ void k_track_predict(EncodeArgs e) {
 }
 
 __global__ void k_stamp(EncodeArgs e) {
+    pdl_enter();
     const ScenParams& sp = e.params[blockIdx.y];
     if ((int)blockIdx.x >= sp.n_tracks) return;
     const int b = sp.b;
@@ -191,6 +196,7 @@ __global__ void k_stamp(EncodeArgs e) {
 }
 
 __global__ void k_set_goal(EncodeArgs e) {
+    pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= e.nscen) return;
     const ScenParams& sp = e.params[k];
@@ -201,6 +207,7 @@ __global__ void k_set_goal(EncodeArgs e) {
 __global__ void k_scatter_tracks(const twg_track* __restrict__ src, const int* __restrict__ off, int nscen,
                                  const int* __restrict__ scen_b, twg_track* __restrict__ dst, int* __restrict__ missed,
                                  int cap) {
+    pdl_enter();
     const int k = blockIdx.y;
     if (k >= nscen) return;
     const int n = off[k + 1] - off[k];
@@ -259,7 +266,9 @@ cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P,
 
 cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nscen, const int* scen_b, twg_track* dst,
                                   int* missed, int cap, cudaStream_t st) {
-    k_scatter_tracks<<<dim3(1, nscen), 128, 0, st>>>(src, off, nscen, scen_b, dst, missed, cap);
+    cudaError_t err = launch_pdl(k_scatter_tracks, dim3(1, nscen), dim3(128), 0, st, src, off, nscen, scen_b, dst,
+                                 missed, cap);
+    if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 
@@ -287,22 +296,23 @@ cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_track
     if (any_cold) {
         dim3 blk(128, 4);
         dim3 grid((unsigned)((e.P + 127) / 128), (e.H + 3) / 4, e.nscen);
-        k_encode_cold<<<grid, blk, 0, st>>>(e);
+        if (cudaError_t err = launch_pdl(k_encode_cold, grid, blk, 0, st, e)) return err;
         ++nl;
     }
     if (max_prev_boxes > 0) {
-        k_unstamp<<<dim3(max_prev_boxes, e.nscen), 256, 0, st>>>(e);
+        if (cudaError_t err = launch_pdl(k_unstamp, dim3(max_prev_boxes, e.nscen), dim3(256), 0, st, e)) return err;
         ++nl;
     }
     const int sb = (e.nscen + 127) / 128;
-    k_goal_reset<<<sb, 128, 0, st>>>(e);
+    if (cudaError_t err = launch_pdl(k_goal_reset, dim3(sb), dim3(128), 0, st, e)) return err;
     ++nl;
     if (max_tracks > 0) {
-        k_track_predict<<<dim3((max_tracks + 63) / 64, e.nscen), 64, 0, st>>>(e);
-        k_stamp<<<dim3(max_tracks, e.nscen), 256, 0, st>>>(e);
+        if (cudaError_t err = launch_pdl(k_track_predict, dim3((max_tracks + 63) / 64, e.nscen), dim3(64), 0, st, e))
+            return err;
+        if (cudaError_t err = launch_pdl(k_stamp, dim3(max_tracks, e.nscen), dim3(256), 0, st, e)) return err;
         nl += 2;
     }
-    k_set_goal<<<sb, 128, 0, st>>>(e);
+    if (cudaError_t err = launch_pdl(k_set_goal, dim3(sb), dim3(128), 0, st, e)) return err;
     ++nl;
     if (n_launch) *n_launch = nl;
     return cudaGetLastError();

@@ -127,6 +127,21 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 }
 
 // Field encoding (include/twg.h): free = sign bit set (value -u), fixed = sign clear.
+// Programmatic dependent launch (sm_90+): a kernel of the relaxation chain is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so it is launched while the previous kernel
+// drains.  pdl_wait: before touching anything the previous kernel wrote.  pdl_trigger: once this
+// CTA has issued its last work, so the successor's CTAs are only scheduled when every CTA of this
+// grid is finishing (triggering at the start lets early successor CTAs crowd some SMs and
+// unbalances the launch).  Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Small kernels of the encode and path chains: wait, then let the successor be scheduled at once.
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
+
 __device__ __forceinline__ bool is_free(float v) { return __float_as_int(v) < 0; }
 
 }  // namespace twg
