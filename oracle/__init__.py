@@ -71,6 +71,8 @@ def lib():
         L.orc_horizon_ring.argtypes = [i32, d, d, d, i32]
         L.orc_relax_jacobi_f32.restype = i32
         L.orc_relax_jacobi_f32.argtypes = [i32, i32, P, P, i32, i32, f32, P]
+        L.orc_relax_lex_f32.restype = i32
+        L.orc_relax_lex_f32.argtypes = [i32, i32, P, P, i32, i32, f32, P]
         L.orc_index_matrix.restype = None
         L.orc_index_matrix.argtypes = [i32, i32, P, P, P]
         L.orc_kalman_update.restype = i32
@@ -254,6 +256,15 @@ def relax_jacobi_f32(cls, u, max_sweeps, check_every=1, tol=0.0):
     return int(s), float(r[0])
 
 
+def relax_lex_f32(cls, u, max_sweeps, check_every=1, tol=0.0):
+    assert u.dtype == np.float32 and u.flags.c_contiguous
+    cls = np.ascontiguousarray(cls, np.uint8)
+    H, W = u.shape
+    r = np.zeros(1, np.float32)
+    s = lib().orc_relax_lex_f32(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol), _p(r))
+    return int(s), float(r[0])
+
+
 def index_matrix(cls, u):
     cls = np.ascontiguousarray(cls, np.uint8)
     u = np.ascontiguousarray(u, np.float32)
@@ -375,7 +386,7 @@ def next_waypoint(pts):
 
 
 def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0.25, kt=1.0,
-              max_len=None, prev=None, jacobi=False, horizon_mode=0, footprint_mode=0):
+              max_len=None, prev=None, jacobi=False, horizon_mode=0, footprint_mode=0, lex=False):
     """One planning tick, Algorithm 1 on the CPU.
 
     prev: None (cold start) or the dict returned by the previous call (warm
@@ -389,7 +400,7 @@ def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0
         u = init_u32(cls)
     else:
         u = init_u32(cls, prev["u"])
-    relax = relax_jacobi_f32 if jacobi else relax_f32
+    relax = relax_jacobi_f32 if jacobi else (relax_lex_f32 if lex else relax_f32)
     sweeps, res = relax(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol)
     if max_len is None:
         max_len = 4 * (scene.W + scene.H)

@@ -397,6 +397,37 @@ int32_t orc_jacobi_f64(int32_t W, int32_t H, const uint8_t* cls, double* u,
     return s;
 }
 
+/* Lexicographic Gauss-Seidel, Eq. 2 literally, in fp32: rows
+ * y = 0..H-1, columns x = 0..W-1, in place, so W (x - 1) and N (y - 1) are this sweep's values and
+ * E, S the previous sweep's; 0.25 * ((E + W) + (N + S)); residual and stop rule as orc_relax_f32. */
+int32_t orc_relax_lex_f32(int32_t W, int32_t H, const uint8_t* cls, float* u, int32_t max_sweeps,
+                          int32_t check_every, float tol, float* res_out)
+{
+    float res = 0.0f;
+    int32_t s = 0;
+    if (check_every < 1) check_every = 1;
+    for (s = 1; s <= max_sweeps; ++s) {
+        res = 0.0f;
+        for (int32_t y = 0; y < H; ++y)
+            for (int32_t x = 0; x < W; ++x) {
+                size_t q = (size_t)y * W + x;
+                if (cls[q] != ORC_FREE) continue;
+                float uE = x + 1 < W ? u[q + 1] : 0.0f;
+                float uW = x > 0 ? u[q - 1] : 0.0f;
+                float uN = y > 0 ? u[q - W] : 0.0f;
+                float uS = y + 1 < H ? u[q + W] : 0.0f;
+                float nv = 0.25f * ((uE + uW) + (uN + uS));
+                float d = fabsf(nv - u[q]);
+                if (d > res) res = d;
+                u[q] = nv;
+            }
+        if ((s % check_every == 0 && res < tol) || s == max_sweeps) break;
+    }
+    if (max_sweeps <= 0) { s = 0; res = 0.0f; }
+    if (res_out) *res_out = res;
+    return s;
+}
+
 /* Jacobi, Eq. 1 literally, in fp32: every free cell from the previous
  * iterate, 0.25 * ((E + W) + (N + S)); residual and stop rule as orc_relax_f32. */
 int32_t orc_relax_jacobi_f32(int32_t W, int32_t H, const uint8_t* cls, float* u, int32_t max_sweeps,

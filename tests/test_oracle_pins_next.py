@@ -224,3 +224,40 @@ def test_p19_ring_horizon_in_classify(orc):
     assert t[0] == tt
     assert j[0] == min(20, round(tt * sc.warp.warp_spacing / (0.4 * sc.warp.dt)))
     assert abs(p[0, 0] - (3.0 - 0.2 * j[0] * sc.warp.dt)) < 1e-12
+
+
+# --------------------------------------------------------------------- P24 (f3 lexicographic)
+def test_p24_lex_first_sweeps_by_hand(orc):
+    # 1 x 3 strip, goal at x=0, cold 1/2: x=1 sees the goal (W) and the old 1/2 (E): 3/8; x=2 sees
+    # the new 3/8 (W): 3/32.  Sweep 2: x=1: (1 + 3/32)/4 = 35/128; x=2: (35/128)/4 = 35/512.
+    cls = np.array([[orc.GOAL, 0, 0]], np.uint8)
+    u = orc.init_u32(cls)
+    assert orc.relax_lex_f32(cls, u, 1) == (1, 0.40625) and u.tolist() == [[1.0, 0.375, 0.09375]]
+    s, r = orc.relax_lex_f32(cls, u, 1)
+    assert u.tolist() == [[1.0, 35 / 128, 35 / 512]] and r == pytest.approx(0.375 - 35 / 128, abs=0)
+    # a 2 x 2 block: (0,0) goal; (1,0) from W=1 (new), S old 1/2; (0,1) from N=1 (new), E old 1/2;
+    # (1,1) from W, N new: ((0 + 3/8) + (3/8 + 0)) / 4 = 3/16
+    cls = np.zeros((2, 2), np.uint8); cls[0, 0] = orc.GOAL
+    u = orc.init_u32(cls)
+    orc.relax_lex_f32(cls, u, 1)
+    assert u.tolist() == [[1.0, 0.375], [0.375, 0.1875]]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_p24_lex_converges_to_dense_solve(orc, seed):
+    from test_oracle_pins import _direct_solve
+    static, g, _ = random_small_map(700 + seed, 16 + 4 * seed, n_disks=(1, 3), n_walls=(0, 1))
+    cls = static.copy(); cls[g[1], g[0]] = orc.GOAL
+    u = orc.init_u32(cls)
+    orc.relax_lex_f32(cls, u, 100_000, 1, 1e-9)
+    ref = _direct_solve(cls, orc.init_u64(cls))
+    assert np.max(np.abs(u - ref)) < 2e-5
+
+
+def test_p24_lex_spectral_radius(orc):
+    # lexicographic Gauss-Seidel contracts by cos^2(pi / (N + 1)) per sweep (model problem)
+    N = 16
+    cls = np.zeros((N, N), np.uint8)
+    u = np.full((N, N), 0.5, np.float32)
+    res = [orc.relax_lex_f32(cls, u, 1)[1] for _ in range(200)]
+    assert abs(res[-1] / res[-2] - math.cos(math.pi / (N + 1)) ** 2) < 2e-3
