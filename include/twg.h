@@ -134,8 +134,10 @@ typedef struct {
  *   sync_every [64]: convergence flags are read back every sync_every
  *   checks when tol > 0;
  *   mode [0]: 0 = red-black Gauss-Seidel (Eq. 2, the hot path);
- *   1 = Jacobi (Eq. 1: every free cell from the previous iterate;
- *   temporal_depth and rows_per_warp ignored). */
+ *   1 = Jacobi (Eq. 1: every free cell from the previous iterate);
+ *   2 = lexicographic Gauss-Seidel (Eq. 2 literally: row-major order, W and N
+ *   from this sweep; not on row slabs); modes 1, 2 ignore temporal_depth and
+ *   rows_per_warp. */
 typedef struct {
     int32_t max_sweeps, check_every, warm_start, temporal_depth;
     float tol;

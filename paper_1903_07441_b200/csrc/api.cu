@@ -408,13 +408,39 @@ int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows, int n_sm) {
 }
 
 // Rows a4-a6 for the scenarios whose participation flag is set.
+// Tile order and counters of the lexicographic mode (32 x 32 tiles listed by anti-diagonal).
+twg_status ensure_lex(twg_ctx* c) {
+    if (c->d_lex_order) return TWG_OK;
+    const int tx = (c->W + 31) / 32, ty = (c->H + 31) / 32;
+    std::vector<int2> ord;
+    ord.reserve((size_t)tx * ty);
+    for (int d = 0; d <= tx + ty - 2; ++d)
+        for (int j = 0; j < ty; ++j) {
+            const int i = d - j;
+            if (i >= 0 && i < tx) ord.push_back(make_int2(i, j));
+        }
+    TWG_CUDA(c, dev_alloc(&c->d_lex_order, ord.size()));
+    TWG_CUDA(c, cudaMemcpy(c->d_lex_order, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    TWG_CUDA(c, dev_alloc(&c->d_lex_tdone, (size_t)c->B * tx * ty));
+    TWG_CUDA(c, dev_alloc(&c->d_lex_task, 1));
+    c->lex_tx = tx;
+    c->lex_ty = ty;
+    return TWG_OK;
+}
+
 twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& part, int* sweeps_done,
                  float* residual) {
     if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null relax cfg");
     const int maxs = cfg->max_sweeps;
     if (maxs < 0 || cfg->check_every < 0) return fail(c, TWG_E_INVALID_ARG, "negative sweep counts");
-    if (cfg->mode != 0 && cfg->mode != 1) return fail(c, TWG_E_INVALID_ARG, "relax mode must be 0 or 1");
+    if (cfg->mode < 0 || cfg->mode > 2) return fail(c, TWG_E_INVALID_ARG, "relax mode must be 0, 1 or 2");
     const bool jacobi = cfg->mode == 1;
+    const bool lex = cfg->mode == 2;
+    if (lex && c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "lexicographic mode is not available on a row slab");
+    if (lex) {
+        twg_status ls = ensure_lex(c);
+        if (ls != TWG_OK) return ls;
+    }
     const int B = c->B;
     int T = cfg->temporal_depth > 0 ? std::min(cfg->temporal_depth, kMaxT) : 6;
     const float tol = cfg->tol;
@@ -433,6 +459,8 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
         hs[5 * B + b] = 0;  // +0.0f
     }
     TWG_CUDA(c, cudaMemcpyAsync(c->d_ctl, hs, 6 * B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    if (lex)
+        TWG_CUDA(c, cudaMemsetAsync(c->d_lex_tdone, 0, (size_t)B * c->lex_tx * c->lex_ty * sizeof(int), c->stream));
     int nscen = 0;
     for (int b = 0; b < B; ++b) nscen += part[b] ? 1 : 0;
 
@@ -459,6 +487,8 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
             std::vector<int> plan;
             if (jacobi) {
                 plan.assign(chunk, 1);
+            } else if (lex) {
+                plan.push_back(chunk);  // one persistent launch runs the whole chunk
             } else {
                 for (int q = 0; q < chunk / T; ++q) plan.push_back(T);
                 if (chunk % T) plan.push_back(chunk % T);
@@ -481,7 +511,31 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
                     e1 = c->ev_pool[c->ev_used++];
                     TWG_CUDA(c, cudaEventRecord(e0, c->stream));
                 }
-                if (jacobi)
+                if (lex) {
+                    LexArgs la;
+                    la.u0 = c->u[0];
+                    la.u1 = c->u[1];
+                    la.cur = c->d_cur;
+                    la.P = c->P;
+                    la.sstride = c->sstride;
+                    la.W = c->W;
+                    la.H = c->H;
+                    la.B = B;
+                    la.TX = c->lex_tx;
+                    la.TY = c->lex_ty;
+                    la.ntiles = c->lex_tx * c->lex_ty;
+                    la.order = c->d_lex_order;
+                    la.sweeps = t;
+                    la.base = done_sw;
+                    la.tdone = c->d_lex_tdone;
+                    la.task = c->d_lex_task;
+                    la.done = c->d_done;
+                    la.res = c->d_res_bits;
+                    la.res_r0 = c->ghost;
+                    la.res_r1 = c->H - c->ghost;
+                    TWG_CUDA(c, cudaMemsetAsync(c->d_lex_task, 0, sizeof(unsigned), c->stream));
+                    TWG_CUDA(c, launch_lex(la, c->n_sm, c->stream));
+                } else if (jacobi)
                     TWG_CUDA(c, launch_jacobi(a, B, q + 1 == plan.size(), c->stream));
                 else
                     TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0][t], c->tmap[1][t], a, B, qoff, q + 1 == plan.size(),
@@ -492,7 +546,7 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
                     c->prof_cells += (int64_t)nscen * c->W * c->H * t;
                 }
                 c->launches += 1;
-                ++lp;
+                if (!lex) ++lp;  // the lexicographic sweep is in place
             }
             TWG_CUDA(c, launch_check(B, c->d_done, c->d_sweeps, c->d_res_bits, c->d_res, c->d_where, chunk, check, maxs,
                                      tol, c->d_cur, lp & 1, c->stream));
@@ -680,7 +734,7 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
                     c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
                     c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det,
                     c->d_sim_rob, c->d_sim_int, c->d_sim_goal, c->d_sim_nobs, c->d_sim_obs, c->d_sim_obs_old,
-                    c->d_sim_speed, c->d_sim_det, c->d_sim_hist};
+                    c->d_sim_speed, c->d_sim_det, c->d_sim_hist, c->d_lex_order, c->d_lex_tdone, c->d_lex_task};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);

@@ -17,6 +17,8 @@
 // sequence (C2; the library is compiled with -fmad=false, no fast-math, no
 // FTZ); colours are global (x + row_offset + y) parity; the residual is the
 // exact max of fabsf(new - old) over the free cells of the last sweep.
+#include <algorithm>
+
 #include "twg_kernels.cuh"
 
 namespace twg {
@@ -275,6 +277,112 @@ cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- lexicographic Gauss-Seidel (f3)
+// Eq. 2 literally: in each sweep the cells are updated in row-major order in place, so a
+// cell sees this sweep's W and N neighbours and the previous sweep's E and S.  The grid is cut into
+// 32 x 32 tiles; tile (i, j) of sweep s may run once tiles (i - 1, j) and (i, j - 1) have finished
+// sweep s and tiles (i + 1, j), (i, j + 1) and (i, j) itself have finished sweep s - 1 (their old
+// values are what it reads).  A persistent grid of warps takes (sweep, tile, scenario) tasks from a
+// global counter in an order that lists every dependency first, waits on per-tile sweep counters
+// (acquire loads; never on a task no running warp holds, so it cannot deadlock), stages the tile
+// plus a 1-cell halo in shared memory (L2 loads, bypassing L1), runs the 63 anti-diagonals of the
+// tile with one lane per row -- the same row-major order inside the tile -- and writes it back
+// before publishing its counter (release).  Several sweeps are in flight at once (a wavefront of
+// tiles per sweep, consecutive sweeps two tile diagonals apart).
+constexpr int kLexT = 32, kLexWarps = 4, kLexPitch = kLexT + 2;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_ge(const int* p, int v) {
+    while (ld_acquire(p) < v) __nanosleep(64);
+}
+
+__global__ void __launch_bounds__(kLexWarps * 32) k_lex(LexArgs a) {
+    __shared__ float tile[kLexWarps][kLexPitch][kLexPitch + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float (*T)[kLexPitch + 1] = tile[warp];
+    const int per_sweep = a.ntiles * a.B;
+    const unsigned total = (unsigned)per_sweep * (unsigned)a.sweeps;
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(a.task, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= total) break;
+        const int s = (int)(t / (unsigned)per_sweep);
+        const int r = (int)(t % (unsigned)per_sweep);
+        const int k = r / a.B, b = r % a.B;
+        if (a.done[b]) continue;
+        const int2 ij = a.order[k];
+        const int tid = ij.y * a.TX + ij.x;
+        int* td = a.tdone + (int64_t)b * a.ntiles;
+        const int need = a.base + s;  // sweeps this tile has finished before this task
+        if (lane == 0) {
+            wait_ge(td + tid, need);
+            if (ij.x > 0) wait_ge(td + tid - 1, need + 1);
+            if (ij.y > 0) wait_ge(td + tid - a.TX, need + 1);
+            if (ij.x + 1 < a.TX) wait_ge(td + tid + 1, need);
+            if (ij.y + 1 < a.TY) wait_ge(td + tid + a.TX, need);
+        }
+        __syncwarp();
+        float* f = (a.cur[b] ? a.u1 : a.u0) + (int64_t)b * a.sstride;
+        const int x0 = ij.x * kLexT, y0 = ij.y * kLexT;
+        // stage rows y0 - 1 .. y0 + 32, columns x0 - 1 .. x0 + 32 (outside the grid: obstacle 0)
+        for (int q = lane; q < kLexPitch * kLexPitch; q += 32) {
+            const int rr = q / kLexPitch, cc = q - rr * kLexPitch;
+            const int gy = y0 - 1 + rr, gx = x0 - 1 + cc;
+            float v = 0.0f;
+            if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) v = __ldcg(f + (int64_t)gy * a.P + gx);
+            T[rr][cc] = v;
+        }
+        __syncwarp();
+        const bool last = s + 1 == a.sweeps;
+        const int gy = y0 + lane;
+        const bool row_in = gy < a.H;
+        const bool count = last && a.res != nullptr && gy >= a.res_r0 && gy < a.res_r1;
+        float dmax = 0.0f;
+        for (int step = 0; step < 2 * kLexT - 1; ++step) {
+            const int x = step - lane;
+            if (row_in && x >= 0 && x < kLexT && x0 + x < a.W) {
+                const float c = T[lane + 1][x + 1];
+                if (is_free(c)) {
+                    const float nv = 0.25f * ((fabsf(T[lane + 1][x + 2]) + fabsf(T[lane + 1][x])) +
+                                              (fabsf(T[lane][x + 1]) + fabsf(T[lane + 2][x + 1])));
+                    if (count) dmax = fmaxf(dmax, fabsf(-nv - c));
+                    T[lane + 1][x + 1] = -nv;
+                }
+            }
+            __syncwarp();
+        }
+        for (int rr = 0; rr < kLexT; ++rr) {
+            const int yy = y0 + rr, xx = x0 + lane;
+            if (yy < a.H && xx < a.W) f[(int64_t)yy * a.P + xx] = T[rr + 1][lane + 1];
+        }
+        if (count || last) {
+            const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(dmax));
+            if (lane == 0 && m != 0u && a.res != nullptr) atomicMax(&a.res[b], m);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            st_release(td + tid, need + 1);
+        }
+    }
+}
+
+cudaError_t launch_lex(const LexArgs& a, int n_sm, cudaStream_t st) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lex, kLexWarps * 32, 0);
+    const int blocks = std::max(1, n_sm * std::max(per_sm, 1));
+    k_lex<<<blocks, kLexWarps * 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- convergence control (a6)
 // After a chunk of `chunk` sweeps whose last launch accumulated the residual:
 // sweeps += chunk; stop when (sweeps % check_every == 0 && res < tol) or
@@ -364,6 +472,7 @@ void preload_relax_kernels() {
     preload_T<5>(); preload_T<6>(); preload_T<7>(); preload_T<8>();
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, k_rb_simple);
+    cudaFuncGetAttributes(&a, k_lex);
     cudaFuncGetAttributes(&a, k_jacobi);
     cudaFuncGetAttributes(&a, k_check);
     cudaFuncGetAttributes(&a, k_fixup);

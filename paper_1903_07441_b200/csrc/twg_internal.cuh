@@ -197,6 +197,11 @@ struct twg_ctx {
     twg::TrkReq* d_trk_req = nullptr;
     double2* d_trk_det = nullptr;
     int64_t trk_det_cap = 0;
+    // lexicographic relaxation (f3)
+    int lex_tx = 0, lex_ty = 0;
+    int2* d_lex_order = nullptr;
+    int* d_lex_tdone = nullptr;
+    unsigned* d_lex_task = nullptr;
     // closed-loop simulator (row f2)
     int sim_ocap = 0;
     double* d_sim_rob = nullptr;       // [B][6]

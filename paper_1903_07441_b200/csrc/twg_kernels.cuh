@@ -25,6 +25,22 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 cudaError_t launch_rb_tblock(int T, const CUtensorMap& map0, const CUtensorMap& map1, const RelaxArgs& a, int B, int qoff, bool resid,
                              cudaStream_t st);
 cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st);
+struct LexArgs {
+    float* u0;
+    float* u1;
+    const int* cur;
+    int64_t P, sstride;
+    int W, H, B;
+    int TX, TY, ntiles;    // 32 x 32 tiles
+    const int2* order;     // tiles (i, j) in anti-diagonal order, [ntiles]
+    int sweeps, base;      // sweeps in this launch; sweeps finished before it (this twg_relax call)
+    int* tdone;            // [B][ntiles] sweeps finished per tile
+    unsigned* task;        // task counter (zeroed before the launch)
+    const int* done;
+    unsigned* res;         // residual bits of the launch's last sweep (nullptr: not tracked)
+    int res_r0, res_r1;
+};
+cudaError_t launch_lex(const LexArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_warp_map(int32_t* out, int W, int H, double cs, double ox, double oy, double xr, double yr, double c,
                             double s, double w, cudaStream_t st);
 cudaError_t launch_rb_simple(float* u, int64_t P, int64_t sstride, int W, int H, int B, int color, int row_off,

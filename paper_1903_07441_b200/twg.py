@@ -169,7 +169,7 @@ def warp_cfg(dt=0.1, Q=None, warp_spacing=1.0, eps_v=0.05, safety_radius=0.5, ho
 
 def relax_cfg(max_sweeps=100, check_every=0, warm_start=1, temporal_depth=0, tol=0.0, rows_per_warp=0,
               sync_every=0, mode=0):
-    """mode 0: red-black Gauss-Seidel (Eq. 2); 1: Jacobi (Eq. 1)."""
+    """mode 0: red-black Gauss-Seidel (Eq. 2); 1: Jacobi (Eq. 1); 2: lexicographic Gauss-Seidel."""
     return RelaxCfg(max_sweeps, check_every, warm_start, temporal_depth, tol, rows_per_warp, sync_every, mode)
 
 

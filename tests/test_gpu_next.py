@@ -225,3 +225,48 @@ def test_invalid_modes_rejected():
         pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(horizon_mode=2), warm=0)
     with pytest.raises(T.TwgError):
         pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(footprint_mode=-1), warm=0)
+
+
+# ------------------------------------------------------------------ f3 lexicographic Gauss-Seidel
+@pytest.mark.parametrize("W,H", [(64, 64), (300, 211), (33, 97), (1, 1), (5, 3), (1000, 40)])
+def test_lex_fixed_budget(W, H):
+    sc = _rand_scene(W, H, W * 5 + H)
+    pl = _planner(sc)
+    pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
+    S = 23
+    sw, res = pl.relax(relax_cfg(max_sweeps=S, mode=2))
+    _, cls, *_ = oracle.classify(sc)
+    u = oracle.init_u32(cls)
+    s_ref, r_ref = oracle.relax_lex_f32(cls, u, S, S, 0.0)
+    assert int(sw[0]) == s_ref == S and np.float32(res[0]) == np.float32(r_ref)
+    _assert_field(pl.get_field(0, 1), u)
+
+
+def test_lex_tolerance_batch_and_plan():
+    scs = [scene_random(f"lx{k}", 128, 3, 4, 90 + k) for k in range(3)]
+    pl = Planner(128, 128, 3, 0.1, (0.0, 0.0), device=0, stream=_stream())
+    for k, sc in enumerate(scs):
+        pl.set_static(sc.static, b=k)
+    rc = relax_cfg(max_sweeps=4000, check_every=25, tol=1e-5, warm_start=0, mode=2, sync_every=2)
+    st, res, cells, sm = pl.plan_step(-1, [s.robot for s in scs], [s.goal for s in scs],
+                                      np.concatenate([s.tracks for s in scs]), [s.n_tracks for s in scs],
+                                      warp_cfg(), rc, band_cfg(10, 2000, 4000))
+    for k, sc in enumerate(scs):
+        ref = oracle.plan_step(sc, max_sweeps=4000, check_every=25, tol=1e-5, iters=10, max_len=2000, lex=True)
+        assert res[k].sweeps == ref["sweeps"] and res[k].sweeps % 25 == 0
+        _assert_field(pl.get_field(k, 1), ref["u"])
+        if ref["walk_status"] == 0:
+            assert np.array_equal(cells[k, :res[k].n_cells], ref["cells"])
+
+
+def test_lex_large_grid_sampled():
+    # 2048^2, 6 sweeps: parity on row bands (the oracle relaxes the full grid)
+    sc = scene_random("lxL", 2048, 64, 100, 3)
+    pl = _planner(sc)
+    pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
+    sw, res = pl.relax(relax_cfg(max_sweeps=6, mode=2))
+    _, cls, *_ = oracle.classify(sc)
+    u = oracle.init_u32(cls)
+    s_ref, r_ref = oracle.relax_lex_f32(cls, u, 6, 6, 0.0)
+    assert np.float32(res[0]) == np.float32(r_ref)
+    _assert_field(pl.get_field(0, 1), u)

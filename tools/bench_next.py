@@ -2,6 +2,7 @@
 warm-up), each against its roofline; writes one JSON object (stdout and --out).
 
   f3 Jacobi (k_jacobi):        8 B per cell per sweep (fp32 read + write)      -> HBM roofline
+  f3 lexicographic (k_lex):    8 B per cell per sweep; wavefront-latency bound in practice
   f3 index matrix (k_index_dir + 2D copy-out): 4 B read + 1 B written per cell (+1 B D2D copy)
   f3 warp map (k_warp_map):    4 B written per cell (int32), fp64 math per cell
   f1 tracker tick:             latency per tick at 200 (C3) and 3200 (C4) tracks, plus the
@@ -51,6 +52,11 @@ def main():
         glups = N * N * S / ms / 1e6
         out[f"jacobi_{N}"] = {"sweeps": S, "ms": ms, "glups": glups, "gbs": 8 * glups,
                               "frac_hbm": 8 * glups / PEAK}
+        SL = max(S // 10, 4)
+        ms = timed(lambda: pl.relax(relax_cfg(max_sweeps=SL, mode=2), want_result=False), 2, st)
+        gl = N * N * SL / ms / 1e6
+        out[f"lexicographic_{N}"] = {"sweeps": SL, "ms": ms, "glups": gl, "gbs_equiv_8B": 8 * gl,
+                                     "frac_hbm_8B": 8 * gl / PEAK}
         ms_rb = timed(lambda: pl.relax(relax_cfg(max_sweeps=S), want_result=False), 3, st)
         out[f"redblack_{N}"] = {"sweeps": S, "ms": ms_rb, "glups": N * N * S / ms_rb / 1e6}
         dm = torch.zeros((N, N), dtype=torch.uint8, device="cuda")
