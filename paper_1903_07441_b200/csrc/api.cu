@@ -408,23 +408,47 @@ int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows, int n_sm) {
 }
 
 // Rows a4-a6 for the scenarios whose participation flag is set.
-// Tile order and counters of the lexicographic mode (32 x 32 tiles listed by anti-diagonal).
-twg_status ensure_lex(twg_ctx* c) {
-    if (c->d_lex_order) return TWG_OK;
-    const int tx = (c->W + 31) / 32, ty = (c->H + 31) / 32;
+// Task lists and counters of the lexicographic mode: 32 x 32 tiles, tasks (sweep s, tile (i, j)) of
+// one launch of `sweeps` sweeps ordered by wavefront time i + j + 2 s, then s, then j.  Every
+// dependency of a task has a smaller time, so the order is topological.  Lists are cached per
+// launch length (a relaxation uses at most two: kLexMaxSweeps and its remainder).
+constexpr int kLexMaxSweeps = 64;  // sweeps per persistent launch
+int2* lex_tasks(twg_ctx* c, int sweeps) {
+    for (auto& e : c->lex_lists)
+        if (e.first == sweeps) return e.second;
+    const int tx = c->lex_tx, ty = c->lex_ty;
     std::vector<int2> ord;
-    ord.reserve((size_t)tx * ty);
-    for (int d = 0; d <= tx + ty - 2; ++d)
-        for (int j = 0; j < ty; ++j) {
-            const int i = d - j;
-            if (i >= 0 && i < tx) ord.push_back(make_int2(i, j));
+    ord.reserve((size_t)tx * ty * sweeps);
+    const int dmax = tx + ty - 2;
+    for (int tau = 0; tau <= dmax + 2 * (sweeps - 1); ++tau)
+        for (int s = 0; s < sweeps; ++s) {
+            const int d = tau - 2 * s;
+            if (d < 0 || d > dmax) continue;
+            for (int j = 0; j < ty; ++j) {
+                const int i = d - j;
+                if (i >= 0 && i < tx) ord.push_back(make_int2(i | (s << 16), j));
+            }
         }
-    TWG_CUDA(c, dev_alloc(&c->d_lex_order, ord.size()));
-    TWG_CUDA(c, cudaMemcpy(c->d_lex_order, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    TWG_CUDA(c, dev_alloc(&c->d_lex_tdone, (size_t)c->B * tx * ty));
+    int2* d = nullptr;
+    if (dev_alloc(&d, ord.size()) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    if (c->lex_lists.size() >= 4) {  // keep a handful
+        cudaFree(c->lex_lists.front().second);
+        c->lex_lists.erase(c->lex_lists.begin());
+    }
+    c->lex_lists.emplace_back(sweeps, d);
+    return d;
+}
+
+twg_status ensure_lex(twg_ctx* c) {
+    if (c->d_lex_tdone) return TWG_OK;
+    c->lex_tx = (c->W + 31) / 32;
+    c->lex_ty = (c->H + 31) / 32;
+    TWG_CUDA(c, dev_alloc(&c->d_lex_tdone, (size_t)c->B * c->lex_tx * c->lex_ty));
     TWG_CUDA(c, dev_alloc(&c->d_lex_task, 1));
-    c->lex_tx = tx;
-    c->lex_ty = ty;
     return TWG_OK;
 }
 
@@ -480,6 +504,7 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
         a.res_r1 = c->H - c->ghost;
         const int qoff = c->row_off & 1;
         int done_sw = 0, nchunk = 0;
+        int lex_base = 0;  // sweeps finished by earlier lexicographic launches of this call
         while (done_sw < maxs) {
             const int chunk = std::min(check, maxs - done_sw);
             // launches of T sweeps, then the remainder; the last launch accumulates the residual (the
@@ -488,7 +513,8 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
             if (jacobi) {
                 plan.assign(chunk, 1);
             } else if (lex) {
-                plan.push_back(chunk);  // one persistent launch runs the whole chunk
+                for (int q = 0; q < chunk / kLexMaxSweeps; ++q) plan.push_back(kLexMaxSweeps);  // persistent launches
+                if (chunk % kLexMaxSweeps) plan.push_back(chunk % kLexMaxSweeps);
             } else {
                 for (int q = 0; q < chunk / T; ++q) plan.push_back(T);
                 if (chunk % T) plan.push_back(chunk % T);
@@ -512,6 +538,8 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
                     TWG_CUDA(c, cudaEventRecord(e0, c->stream));
                 }
                 if (lex) {
+                    int2* tl = lex_tasks(c, t);
+                    if (!tl) return fail(c, TWG_E_NO_MEMORY, "lexicographic task list");
                     LexArgs la;
                     la.u0 = c->u[0];
                     la.u1 = c->u[1];
@@ -524,13 +552,15 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
                     la.TX = c->lex_tx;
                     la.TY = c->lex_ty;
                     la.ntiles = c->lex_tx * c->lex_ty;
-                    la.order = c->d_lex_order;
+                    la.tasks = tl;
+                    la.ntasks = t * c->lex_tx * c->lex_ty;
                     la.sweeps = t;
-                    la.base = done_sw;
+                    la.base = lex_base;
+                    lex_base += t;
                     la.tdone = c->d_lex_tdone;
                     la.task = c->d_lex_task;
                     la.done = c->d_done;
-                    la.res = c->d_res_bits;
+                    la.res = q + 1 == plan.size() ? c->d_res_bits : nullptr;  // the chunk's last sweep only
                     la.res_r0 = c->ghost;
                     la.res_r1 = c->H - c->ghost;
                     TWG_CUDA(c, cudaMemsetAsync(c->d_lex_task, 0, sizeof(unsigned), c->stream));
@@ -734,9 +764,10 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
                     c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
                     c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det,
                     c->d_sim_rob, c->d_sim_int, c->d_sim_goal, c->d_sim_nobs, c->d_sim_obs, c->d_sim_obs_old,
-                    c->d_sim_speed, c->d_sim_det, c->d_sim_hist, c->d_lex_order, c->d_lex_tdone, c->d_lex_task};
+                    c->d_sim_speed, c->d_sim_det, c->d_sim_hist, c->d_lex_tdone, c->d_lex_task};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (auto& e : c->lex_lists) cudaFree(e.second);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;

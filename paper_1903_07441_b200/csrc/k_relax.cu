@@ -283,7 +283,8 @@ cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st
 // 32 x 32 tiles; tile (i, j) of sweep s may run once tiles (i - 1, j) and (i, j - 1) have finished
 // sweep s and tiles (i + 1, j), (i, j + 1) and (i, j) itself have finished sweep s - 1 (their old
 // values are what it reads).  A persistent grid of warps takes (sweep, tile, scenario) tasks from a
-// global counter in an order that lists every dependency first, waits on per-tile sweep counters
+// global counter in wavefront-time order (tile diagonal + 2 sweep, so consecutive sweeps overlap and
+// every dependency is listed first), waits on per-tile sweep counters
 // (acquire loads; never on a task no running warp holds, so it cannot deadlock), stages the tile
 // plus a 1-cell halo in shared memory (L2 loads, bypassing L1), runs the 63 anti-diagonals of the
 // tile with one lane per row -- the same row-major order inside the tile -- and writes it back
@@ -291,54 +292,67 @@ cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st
 // tiles per sweep, consecutive sweeps two tile diagonals apart).
 constexpr int kLexT = 32, kLexWarps = 4, kLexPitch = kLexT + 2;
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+__device__ __forceinline__ int ld_relaxed(const int* p) {
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void wait_ge(const int* p, int v) {
-    while (ld_acquire(p) < v) __nanosleep(64);
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __global__ void __launch_bounds__(kLexWarps * 32) k_lex(LexArgs a) {
     __shared__ float tile[kLexWarps][kLexPitch][kLexPitch + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float (*T)[kLexPitch + 1] = tile[warp];
-    const int per_sweep = a.ntiles * a.B;
-    const unsigned total = (unsigned)per_sweep * (unsigned)a.sweeps;
+    const unsigned total = (unsigned)a.ntasks * (unsigned)a.B;
+    constexpr int kStage = (kLexPitch * kLexPitch + 31) / 32;
     for (;;) {
         unsigned t = 0;
         if (lane == 0) t = atomicAdd(a.task, 1u);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= total) break;
-        const int s = (int)(t / (unsigned)per_sweep);
-        const int r = (int)(t % (unsigned)per_sweep);
-        const int k = r / a.B, b = r % a.B;
+        const int b = (int)(t % (unsigned)a.B);
         if (a.done[b]) continue;
-        const int2 ij = a.order[k];
-        const int tid = ij.y * a.TX + ij.x;
+        const int2 tk = a.tasks[t / (unsigned)a.B];  // (i | s << 16, j)
+        const int ti = tk.x & 0xffff, s = tk.x >> 16, tj = tk.y;
+        const int tid = tj * a.TX + ti;
         int* td = a.tdone + (int64_t)b * a.ntiles;
         const int need = a.base + s;  // sweeps this tile has finished before this task
-        if (lane == 0) {
-            wait_ge(td + tid, need);
-            if (ij.x > 0) wait_ge(td + tid - 1, need + 1);
-            if (ij.y > 0) wait_ge(td + tid - a.TX, need + 1);
-            if (ij.x + 1 < a.TX) wait_ge(td + tid + 1, need);
-            if (ij.y + 1 < a.TY) wait_ge(td + tid + a.TX, need);
+        // lanes 0..4 poll the five counters together (one L2 round trip per poll), then a fence
+        // orders the staging loads after what was observed
+        const int* dp = td + tid;
+        int dv = need;
+        bool has = lane == 0;
+        if (lane == 1) { has = ti > 0; dp = td + tid - 1; dv = need + 1; }
+        if (lane == 2) { has = tj > 0; dp = td + tid - a.TX; dv = need + 1; }
+        if (lane == 3) { has = ti + 1 < a.TX; dp = td + tid + 1; }
+        if (lane == 4) { has = tj + 1 < a.TY; dp = td + tid + a.TX; }
+        unsigned ns = 32;  // exponential back-off keeps the polling of waiting warps off the L2
+        while (!__all_sync(0xffffffffu, !has || ld_relaxed(dp) >= dv)) {
+            __nanosleep(ns);
+            ns = min(ns * 2u, 512u);
         }
-        __syncwarp();
+        __threadfence();
         float* f = (a.cur[b] ? a.u1 : a.u0) + (int64_t)b * a.sstride;
-        const int x0 = ij.x * kLexT, y0 = ij.y * kLexT;
-        // stage rows y0 - 1 .. y0 + 32, columns x0 - 1 .. x0 + 32 (outside the grid: obstacle 0)
-        for (int q = lane; q < kLexPitch * kLexPitch; q += 32) {
+        const int x0 = ti * kLexT, y0 = tj * kLexT;
+        // stage rows y0 - 1 .. y0 + 32, columns x0 - 1 .. x0 + 32 (outside the grid: obstacle 0):
+        // all loads first (L2, bypassing the non-coherent L1), then the shared-memory stores
+        float v[kStage];
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+            const int q = lane + 32 * k;
             const int rr = q / kLexPitch, cc = q - rr * kLexPitch;
             const int gy = y0 - 1 + rr, gx = x0 - 1 + cc;
-            float v = 0.0f;
-            if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) v = __ldcg(f + (int64_t)gy * a.P + gx);
-            T[rr][cc] = v;
+            v[k] = (q < kLexPitch * kLexPitch && gy >= 0 && gy < a.H && gx >= 0 && gx < a.W)
+                       ? __ldcg(f + (int64_t)gy * a.P + gx)
+                       : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+            const int q = lane + 32 * k;
+            const int rr = q / kLexPitch, cc = q - rr * kLexPitch;
+            if (q < kLexPitch * kLexPitch) T[rr][cc] = v[k];
         }
         __syncwarp();
         const bool last = s + 1 == a.sweeps;
@@ -363,22 +377,22 @@ __global__ void __launch_bounds__(kLexWarps * 32) k_lex(LexArgs a) {
             const int yy = y0 + rr, xx = x0 + lane;
             if (yy < a.H && xx < a.W) f[(int64_t)yy * a.P + xx] = T[rr + 1][lane + 1];
         }
-        if (count || last) {
+        if (last) {
             const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(dmax));
             if (lane == 0 && m != 0u && a.res != nullptr) atomicMax(&a.res[b], m);
         }
+        __threadfence();  // every lane's tile stores before the counter
         __syncwarp();
-        if (lane == 0) {
-            __threadfence();
-            st_release(td + tid, need + 1);
-        }
+        if (lane == 0) st_relaxed(td + tid, need + 1);
     }
 }
 
 cudaError_t launch_lex(const LexArgs& a, int n_sm, cudaStream_t st) {
+    // 8 warps per SM: the wavefront exposes a few thousand ready tasks at most, and every extra
+    // waiting warp only adds polling
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lex, kLexWarps * 32, 0);
-    const int blocks = std::max(1, n_sm * std::max(per_sm, 1));
+    const int blocks = std::max(1, n_sm * std::min(std::max(per_sm, 1), 2));
     k_lex<<<blocks, kLexWarps * 32, 0, st>>>(a);
     return cudaGetLastError();
 }

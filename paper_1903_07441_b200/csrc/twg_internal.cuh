@@ -199,7 +199,7 @@ struct twg_ctx {
     int64_t trk_det_cap = 0;
     // lexicographic relaxation (f3)
     int lex_tx = 0, lex_ty = 0;
-    int2* d_lex_order = nullptr;
+    std::vector<std::pair<int, int2*>> lex_lists;  // task lists per launch length
     int* d_lex_tdone = nullptr;
     unsigned* d_lex_task = nullptr;
     // closed-loop simulator (row f2)

@@ -32,7 +32,8 @@ struct LexArgs {
     int64_t P, sstride;
     int W, H, B;
     int TX, TY, ntiles;    // 32 x 32 tiles
-    const int2* order;     // tiles (i, j) in anti-diagonal order, [ntiles]
+    const int2* tasks;     // [ntasks] (i | s << 16, j) in wavefront-time order (diag + 2 s)
+    int ntasks;            // sweeps * ntiles
     int sweeps, base;      // sweeps in this launch; sweeps finished before it (this twg_relax call)
     int* tdone;            // [B][ntiles] sweeps finished per tile
     unsigned* task;        // task counter (zeroed before the launch)

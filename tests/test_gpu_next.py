@@ -106,7 +106,7 @@ def test_jacobi_invalid_mode():
     pl = _planner(sc)
     pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
     with pytest.raises(T.TwgError):
-        pl.relax(relax_cfg(max_sweeps=3, mode=2))
+        pl.relax(relax_cfg(max_sweeps=3, mode=3))
 
 
 # ------------------------------------------------------------------ f3 index matrix
