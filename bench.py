@@ -228,6 +228,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         l0 = pl.kernel_launches()
         walk = []
+        d2h = []
         torch.cuda.nvtx.range_push("timed_region_host" if host else "timed_region")
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
@@ -235,6 +236,9 @@ def run_ours(args):
             _, r, _, _ = one(args.warmup + k, host)
             ev[k][1].record(stream)
             walk.append(r[0].walk_status)
+            # read back per step: PathMeta (32 B) + [sweeps|where|res bits|res|flags] (20 B) + the
+            # produced cells (8 B each) and smoothed points (8 B each, up to max_smooth)
+            d2h.append(52 + 8 * r[0].n_cells + 8 * min(r[0].n_smooth, bc.max_smooth) if host else 52)
         torch.cuda.synchronize(dev)
         torch.cuda.nvtx.range_pop()
         launches = pl.kernel_launches() - l0
@@ -244,6 +248,7 @@ def run_ours(args):
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             torch.distributed.barrier()
             ms = float(tt.item())
+        timed_loop.d2h = d2h
         return ms, launches, walk
 
     with Clocks(local, enabled=not args.no_clocks) as clk:
@@ -256,6 +261,7 @@ def run_ours(args):
     rms, rl, rcells = pl.profile_read()
     pl.profile(0)
     ms_e2e, _, _ = timed_loop(host=True)
+    d2h_e2e = int(round(sum(timed_loop.d2h) / max(len(timed_loop.d2h), 1)))
 
     # kernel-only relaxation throughput (S = relax_sweeps), same field
     rc_big = relax_cfg(max_sweeps=args.relax_sweeps, warm_start=1, temporal_depth=args.T, rows_per_warp=args.rows)
@@ -300,8 +306,8 @@ def run_ours(args):
                      "kernel_share_of_step": (rms / ms_prof) if ms_prof else None,
                      "events": "per-launch CUDA events on the library stream, profiled pass of the same steps",
                      "effective_glups_vs_8B_per_LUP": (rcells / (rms * 1e-3) / 1e9) / (peak / 8.0) if rms else None},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(sc0.n_tracks * 160 + 40),
-                "d2h_bytes_per_step": int(bc.max_len * 8 + bc.max_smooth * 8 + 32), "ms_per_step": ms_e2e / args.steps},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(sc0.n_tracks * 160 + 480),  # tracks + parameter and control blocks
+                "d2h_bytes_per_step": d2h_e2e, "ms_per_step": ms_e2e / args.steps},
         "gpu_launches": int(launches),
         "walk_ok_steps": int(sum(1 for w in walk if w == 0)),
         "prep": prep,

@@ -278,7 +278,7 @@ TWG_API twg_status twg_extract_path(twg_ctx* ctx, int32_t b, const twg_band_cfg*
  *   concatenation of n_tracks[0..batch) tracks, out[batch],
  *   cells_xy[batch][2 max_len], smooth_xy[batch][2 max_smooth].
  * tracks may be host or device; every other pointer is host (cells_xy,
- * smooth_xy may be NULL).  tracks = NULL and n_tracks = NULL: every
+ * smooth_xy may be NULL; for b >= 0 only the entries produced are written).  tracks = NULL and n_tracks = NULL: every
  * scenario uses its resident tracker table (row f1).
  * Returns the worst per-scenario status. */
 TWG_API twg_status twg_plan_step(twg_ctx* ctx, int32_t b, const twg_robot* robot, const int32_t* goal_xy,

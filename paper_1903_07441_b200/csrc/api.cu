@@ -894,25 +894,34 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
     int* hf = hsw + 4 * B;
     TWG_CUDA(c, cudaMemcpyAsync(hm, c->d_meta, mb, cudaMemcpyDeviceToHost, c->stream));
     TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, 5 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    if (cells_xy) {
-        if (b >= 0)
-            TWG_CUDA(c, cudaMemcpyAsync(cells_xy, c->d_cells + (int64_t)b * c->path_len_cap,
-                                        bcfg->max_len * sizeof(int2), cudaMemcpyDeviceToHost, c->stream));
-        else
+    if (b < 0) {  // batch: whole capacity per scenario, one strided copy each
+        if (cells_xy)
             TWG_CUDA(c, cudaMemcpy2DAsync(cells_xy, bcfg->max_len * sizeof(int2), c->d_cells,
                                           c->path_len_cap * sizeof(int2), bcfg->max_len * sizeof(int2), B,
                                           cudaMemcpyDeviceToHost, c->stream));
-    }
-    if (smooth_xy) {
-        if (b >= 0)
-            TWG_CUDA(c, cudaMemcpyAsync(smooth_xy, c->d_smooth + (int64_t)b * c->smooth_cap,
-                                        bcfg->max_smooth * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
-        else
+        if (smooth_xy)
             TWG_CUDA(c, cudaMemcpy2DAsync(smooth_xy, bcfg->max_smooth * sizeof(float2), c->d_smooth,
                                           c->smooth_cap * sizeof(float2), bcfg->max_smooth * sizeof(float2), B,
                                           cudaMemcpyDeviceToHost, c->stream));
     }
     TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (b >= 0 && (cells_xy || smooth_xy) && hm[b].status == TWG_OK) {
+        // one scenario: read back only the cells and points produced, through the pinned staging
+        // buffer (the caller's arrays are usually pageable)
+        const int nc = std::min(hm[b].n_cells, bcfg->max_len);
+        const int nsm = std::min(hm[b].n_smooth, bcfg->max_smooth);
+        const size_t bc = cells_xy ? (size_t)nc * sizeof(int2) : 0, bsm = smooth_xy ? (size_t)nsm * sizeof(float2) : 0;
+        char* hp = nullptr;
+        TWG_CUDA(c, stage_alloc(c, bc + bsm + 16, reinterpret_cast<void**>(&hp)));
+        if (bc) TWG_CUDA(c, cudaMemcpyAsync(hp, c->d_cells + (int64_t)b * c->path_len_cap, bc, cudaMemcpyDeviceToHost,
+                                            c->stream));
+        if (bsm)
+            TWG_CUDA(c, cudaMemcpyAsync(hp + bc, c->d_smooth + (int64_t)b * c->smooth_cap, bsm,
+                                        cudaMemcpyDeviceToHost, c->stream));
+        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (bc) std::memcpy(cells_xy, hp, bc);
+        if (bsm) std::memcpy(smooth_xy, hp + bc, bsm);
+    }
     twg_status worst = TWG_OK;
     for (int k = 0; k < ns; ++k) {
         const int q = bs[k];
