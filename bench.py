@@ -418,9 +418,9 @@ def run_c5(args):
     def inputs(tick):  # scene advance and packing are input generation: done before the timed region
         if tick not in ticks:
             ss = [advance_scene(sc, tick) for sc in scs]
-            ticks[tick] = ([s.robot for s in ss], [s.goal for s in ss],
+            ticks[tick] = (np.array([s.robot for s in ss], np.float64), np.array([s.goal for s in ss], np.int32),
                            torch.from_numpy(np.ascontiguousarray(np.vstack([s.tracks for s in ss]))).pin_memory(),
-                           [s.n_tracks for s in ss])
+                           np.array([s.n_tracks for s in ss], np.int32))
         return ticks[tick]
 
     def step(tick, rc):

@@ -260,7 +260,7 @@ class Planner:
     def plan_step(self, b, robots, goals, tracks, n_tracks, wcfg, rcfg, bcfg, want_paths=True):
         """b >= 0: one scenario; b = -1: all.  tracks: concatenated [sum n, 20] (numpy or CUDA tensor)."""
         nb = 1 if b >= 0 else self.B
-        rob = (Robot * nb)(*[Robot(*[float(v) for v in r]) for r in robots])
+        rob = np.ascontiguousarray(np.asarray(robots, np.float64).reshape(nb, 4))  # twg_robot = 4 doubles
         g = np.ascontiguousarray(np.asarray(goals, np.int32).reshape(nb, 2))
         resident = tracks is None and n_tracks is None
         nt = None if resident else np.ascontiguousarray(np.asarray(n_tracks, np.int32).reshape(nb))
@@ -268,7 +268,7 @@ class Planner:
         out = (PlanResult * nb)()
         cells = np.zeros((nb, bcfg.max_len, 2), np.int32) if want_paths else None
         sm = np.zeros((nb, bcfg.max_smooth, 2), np.float32) if want_paths else None
-        st = lib().twg_plan_step(self.ctx, b, rob, _ptr(g), _ptr(t) if (nt is not None and int(nt.sum())) else None,
+        st = lib().twg_plan_step(self.ctx, b, _ptr(rob), _ptr(g), _ptr(t) if (nt is not None and int(nt.sum())) else None,
                                  _ptr(nt),
                                  C.byref(wcfg), C.byref(rcfg), C.byref(bcfg), out, _ptr(cells), _ptr(sm))
         _check(self.ctx, st, ok=(OK, W_GOAL_SWALLOWED, W_TRUNCATED, E_NO_PATH))
