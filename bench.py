@@ -451,10 +451,21 @@ def run_c5(args):
             torch.cuda.synchronize(dev)
             ms_tot += e0.elapsed_time(e1)
             ok += sum(1 for r in res if r.walk_status == 0)
+    gathered = per
     if ws > 1:
         t = torch.tensor([ms_tot], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_tot = float(t.item())
+        # the only exchange of the batch mode -- one all-gather of the per-scenario
+        # result structs (status, sweeps, path cells, next waypoint) of the last step
+        mine = torch.tensor([[r.walk_status, r.sweeps, r.n_cells, r.next_x, r.next_y] for r in res],
+                            dtype=torch.float64, device=dev)
+        allr = [torch.empty_like(mine) for _ in range(ws)]
+        torch.distributed.all_gather(allr, mine)
+        gathered = sum(int(a.shape[0]) for a in allr)
+        okt = torch.tensor([ok], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(okt)
+        ok = int(okt.item())
     value = 512 * 512 * per * ws * args.sweeps * args.steps / (ms_tot * 1e-3) / 1e9
     if rank == 0:
         print(json.dumps({"metric": "harmonic relaxation GLUP/s, batch of 512^2 plan steps", "value": value,
@@ -465,7 +476,8 @@ def run_c5(args):
                                                  f"{per} per rank, warm plan step S={args.sweeps}, "
                                                  f"I={args.band_iters} (host tracks include per-step H2D)"},
                           "scenario_steps_per_s": per * ws * args.steps / (ms_tot * 1e-3),
-                          "walk_ok_fraction": ok / (args.steps * per), "prep_s": prep_s,
+                          "walk_ok_fraction": ok / (args.steps * per * ws), "prep_s": prep_s,
+                          "results_gathered": gathered,
                           "clocks": clk.summary()}), flush=True)
     pl.close()
     if ws > 1:

@@ -355,6 +355,20 @@ TWG_API twg_status twg_sim_tick(twg_ctx* ctx, const twg_sim_cfg* cfg, const twg_
  * heading change in [5k, 5k + 5) degrees), host. */
 TWG_API twg_status twg_sim_histogram(twg_ctx* ctx, int32_t b, int32_t* hist);
 
+/* Descent walk from local cell (x, y) of scenario b on the current field, for
+ * row slabs (the walker is handed from slab to slab).  Follows
+ * Eq. 3 (argmax u over the in-grid 4-neighbours, order +x, -x, +y, -y, C8)
+ * from (x, y), appending every visited cell (local coordinates, the start
+ * included) to cells_xy (host, max_cells pairs), until: the goal
+ * (*code = 0); the next cell lies in a ghost row, i.e. belongs to the
+ * neighbouring slab (*code = 1 above, 2 below; next_xy = that cell, not
+ * appended); an obstacle, no neighbour, or more than max_cells cells
+ * (*code = TWG_E_NO_PATH).  The ghost rows must hold the neighbours' current
+ * rows (exchange them after the last relaxation).  On an unsharded grid the
+ * walk never hands over.  Correctness path, one thread. */
+TWG_API twg_status twg_walk_from(twg_ctx* ctx, int32_t b, int32_t x, int32_t y, int32_t max_cells,
+                                 int32_t* cells_xy, int32_t* n_cells, int32_t* code, int32_t* next_xy);
+
 /* Full-grid index matrix M_idx of scenario b's current field (Eq. 3,
  * P:228-233; Alg. 1): out[height x width] uint8
  * row-major (host or device): 0..3 = step to the in-grid neighbour with the

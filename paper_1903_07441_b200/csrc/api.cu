@@ -1462,6 +1462,34 @@ TWG_API twg_status twg_sim_histogram(twg_ctx* c, int32_t b, int32_t* hist) {
     return TWG_OK;
 }
 
+TWG_API twg_status twg_walk_from(twg_ctx* c, int32_t b, int32_t x, int32_t y, int32_t max_cells, int32_t* cells_xy,
+                                 int32_t* n_cells, int32_t* code, int32_t* next_xy) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (b < 0 || b >= c->B || x < 0 || x >= c->W || y < c->ghost || y >= c->H - c->ghost || max_cells < 0 || !code)
+        return fail(c, TWG_E_INVALID_ARG, "bad argument (the start must lie in the owned rows)");
+    int* d = nullptr;
+    TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&d), (4 + 2 * (size_t)std::max(max_cells, 1)) * sizeof(int),
+                                c->stream));
+    const float* f = c->u[c->cur[b]] + (int64_t)b * c->sstride;
+    TWG_CUDA(c, launch_walk_from(f, c->P, c->W, c->H, c->ghost, c->H - c->ghost, x, y, max_cells, d + 4, d, c->stream));
+    c->launches += 1;
+    int h[4];
+    TWG_CUDA(c, cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (cells_xy && h[1] > 0)
+        TWG_CUDA(c, cudaMemcpy(cells_xy, d + 4, (size_t)h[1] * 2 * sizeof(int), cudaMemcpyDeviceToHost));
+    TWG_CUDA(c, cudaFreeAsync(d, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    *code = h[0];
+    if (n_cells) *n_cells = h[1];
+    if (next_xy) {
+        next_xy[0] = h[2];
+        next_xy[1] = h[3];
+    }
+    return TWG_OK;
+}
+
 TWG_API twg_status twg_index_matrix(twg_ctx* c, int32_t b, uint8_t* out) {
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;

@@ -122,6 +122,8 @@ struct PathArgs {
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
 cudaError_t launch_index_dir(const PathArgs& p, cudaStream_t st);  // k_index_dir alone (twg_index_matrix)
+cudaError_t launch_walk_from(const float* f, int64_t P, int W, int H, int r0, int r1, int x, int y, int max_cells,
+                             int* cells, int* out, cudaStream_t st);
 
 // k_sim.cu (row f2: closed-loop simulator)
 struct SimArgs {

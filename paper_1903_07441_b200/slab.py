@@ -110,6 +110,14 @@ class DistExchanger:
             for r in d.batch_isend_irecv(ops):
                 r.wait()
 
+    def broadcast_from(self, owner: int, values, device=None):
+        """Small int64 message from rank `owner` to every rank (a SUM all-reduce of zeros elsewhere)."""
+        import torch
+        t = torch.tensor(values if self.dist.get_rank() == owner else [0] * len(values), dtype=torch.int64,
+                         device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return [int(v) for v in t.tolist()]
+
     def allreduce_max(self, value: float, device=None) -> float:
         import torch
         t = torch.tensor([value], dtype=torch.float32, device=device)
@@ -156,6 +164,10 @@ class TwgSlabBackend:
         _, res = self.pl.relax(relax_cfg(max_sweeps=n))
         return float(res[0])
 
+    def walk_segment(self, x: int, yl: int, max_cells: int):
+        """Walk from local cell (x, yl) until the goal, a hand-over or a dead end (twg_walk_from)."""
+        return self.pl.walk_from(0, x, yl, max_cells)
+
     def field_view(self):
         import torch
         ptr, pitch = self.pl.field_ptr(0)
@@ -176,6 +188,21 @@ def make_twg_slab(layout: SlabLayout, static_global, robot, goal, tracks, warp, 
     return pl
 
 
+def exchange_local(backends, layouts):
+    """Ghost-row exchange between slabs held by one process (device-to-device copies)."""
+    views = [b.field_view() for b in backends]
+    for r in range(len(backends) - 1):
+        up, dn, lu, ld = views[r], views[r + 1], layouts[r], layouts[r + 1]
+        a, b = lu.owned_bottom()
+        ga, gb = ld.ghost_top()
+        top_src = up[a:b].clone()
+        a2, b2 = ld.owned_top()
+        ga2, gb2 = lu.ghost_bottom()
+        bot_src = dn[a2:b2].clone()
+        dn[ga:gb].copy_(top_src)
+        up[ga2:gb2].copy_(bot_src)
+
+
 def relax_local_slabs(backends, layouts, max_sweeps: int, check_every: int = 0, tol: float = 0.0):
     """All slabs in one process (e.g. several contexts on one GPU): the same interval schedule,
     ghost rows copied between the slabs' buffers, residual = max over slabs."""
@@ -186,17 +213,69 @@ def relax_local_slabs(backends, layouts, max_sweeps: int, check_every: int = 0, 
         if is_check:
             res = max(rs)
         if s < max_sweeps:
-            views = [b.field_view() for b in backends]
-            for r in range(len(backends) - 1):
-                up, dn, lu, ld = views[r], views[r + 1], layouts[r], layouts[r + 1]
-                a, b = lu.owned_bottom()
-                ga, gb = ld.ghost_top()
-                top_src = up[a:b].clone()
-                a2, b2 = ld.owned_top()
-                ga2, gb2 = lu.ghost_bottom()
-                bot_src = dn[a2:b2].clone()
-                dn[ga:gb].copy_(top_src)
-                up[ga2:gb2].copy_(bot_src)
+            exchange_local(backends, layouts)
         if is_check and tol > 0 and check_every > 0 and s % check_every == 0 and res < tol:
             break
     return s, res
+
+
+WALK_GOAL, WALK_UP, WALK_DOWN, WALK_NO_PATH = 0, 1, 2, -5
+
+
+def owner_of_row(H: int, world: int, gy: int) -> int:
+    for r in range(world):
+        r0, r1 = slab_rows(H, world, r)
+        if r0 <= gy < r1:
+            return r
+    raise ValueError(f"row {gy} outside the grid")
+
+
+def sharded_walk(backend, lay: SlabLayout, ex, start, max_len: int, device=None):
+    """Descent walk over row slabs: the rank owning the current cell walks until the
+    goal, a dead end, or the first step into another slab, then hands the walker (next cell and cells
+    so far) to that neighbour with one small message.  Ghost rows are exchanged first so every rank
+    sees its neighbours' final rows.  Returns (code, this rank's cells in global coordinates, total
+    cell count); concatenating the ranks' cells in walk order gives the single-grid walk."""
+    ex.exchange(lay, backend.field_view())
+    x, gy = int(start[0]), int(start[1])
+    owner = owner_of_row(lay.H_global, lay.world, gy)
+    count = 0
+    mine = []
+    while True:
+        if lay.rank == owner:
+            code, seg, nxt = backend.walk_segment(x, gy - lay.row_offset, max_len - count)
+            if code != WALK_NO_PATH and len(seg):
+                seg = np.asarray(seg).copy()
+                seg[:, 1] += lay.row_offset
+                mine.append((count, seg))
+            n = len(seg) if code != WALK_NO_PATH else 0
+            msg = [code, nxt[0] if nxt else -1, (nxt[1] + lay.row_offset) if nxt else -1, count + n]
+        else:
+            msg = [0, 0, 0, 0]
+        code, nx, ny, count = ex.broadcast_from(owner, msg, device)
+        if code == WALK_NO_PATH:
+            return code, [], 0
+        if code == WALK_GOAL:
+            return code, mine, count
+        owner += -1 if code == WALK_UP else 1
+        x, gy = nx, ny
+
+
+def sharded_walk_local(backends, layouts, start, max_len: int):
+    """The same hand-over on several slabs held by one process (ghost rows already exchanged)."""
+    lay0 = layouts[0]
+    x, gy = int(start[0]), int(start[1])
+    owner = owner_of_row(lay0.H_global, lay0.world, gy)
+    cells = []
+    while True:
+        lay = layouts[owner]
+        code, seg, nxt = backends[owner].walk_segment(x, gy - lay.row_offset, max_len - len(cells))
+        if code == WALK_NO_PATH:
+            return code, np.zeros((0, 2), np.int32)
+        seg = np.asarray(seg).copy()
+        seg[:, 1] += lay.row_offset
+        cells.extend(seg.tolist())
+        if code == WALK_GOAL:
+            return code, np.asarray(cells, np.int32)
+        owner += -1 if code == WALK_UP else 1
+        x, gy = nxt[0], nxt[1] + lay.row_offset

@@ -99,6 +99,8 @@ SIGNATURES = [
     ("twg_sim_tick", C.c_int32, [_P, C.POINTER(SimCfg), C.POINTER(WarpCfg), C.POINTER(RelaxCfg), C.POINTER(BandCfg),
                                  C.POINTER(TrackerCfg), _P, C.POINTER(C.c_int32)]),
     ("twg_sim_histogram", C.c_int32, [_P, C.c_int32, _P]),
+    ("twg_walk_from", C.c_int32, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int32), _P]),
     ("twg_index_matrix", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_warp_map", C.c_int32, [_P, C.POINTER(Robot), C.c_double, _P]),
     ("twg_field_ptr", C.c_int32, [_P, C.c_int32, C.POINTER(_P), C.POINTER(C.c_int64)]),
@@ -333,6 +335,17 @@ class Planner:
         h = np.zeros(36, np.int32)
         _check(self.ctx, lib().twg_sim_histogram(self.ctx, b, _ptr(h)))
         return h
+
+    def walk_from(self, b, x, y, max_cells):
+        """twg_walk_from: (code, cells [n, 2] local, next (x, y) local or None); code 0 goal, 1 / 2 handed
+        to the slab above / below, E_NO_PATH."""
+        cells = np.zeros((max(max_cells, 1), 2), np.int32)
+        n, code = C.c_int32(), C.c_int32()
+        nxt = np.zeros(2, np.int32)
+        _check(self.ctx, lib().twg_walk_from(self.ctx, b, int(x), int(y), int(max_cells), _ptr(cells), C.byref(n),
+                                             C.byref(code), _ptr(nxt)))
+        c = code.value
+        return c, cells[: n.value].copy(), (int(nxt[0]), int(nxt[1])) if c in (1, 2) else None
 
     def index_matrix(self, b=0, out=None):
         """twg_index_matrix: uint8 [H, W] M_idx of scenario b (0..3 move, 4 goal, 5 obstacle, 6 none)."""

@@ -10,7 +10,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1903_07441_b200.slab import SlabLayout, SlabRelaxer, DistExchanger, interval_schedule, slab_rows
+from paper_1903_07441_b200.slab import (SlabLayout, SlabRelaxer, DistExchanger, interval_schedule, slab_rows,
+                                        sharded_walk, WALK_GOAL)
 
 
 def _free_port():
@@ -48,6 +49,73 @@ class OracleSlabBackend:
 
     def field_view(self):
         return self.t
+
+    def walk_segment(self, x, yl, max_cells):
+        """Follow the oracle's index matrix of the local grid inside the owned rows (test backend)."""
+        m = self.o.index_matrix(self.cls, self.u)
+        lay = self.lay
+        cells = [(x, yl)]
+        steps = ((1, 0), (-1, 0), (0, 1), (0, -1))
+        if max_cells < 1:
+            return -5, [], None
+        while True:
+            d = int(m[yl, x])
+            if d == 4:
+                return 0, cells, None
+            if d >= 5:
+                return -5, [], None
+            nx, ny = x + steps[d][0], yl + steps[d][1]
+            if ny < lay.G or ny >= lay.local_h - lay.G:
+                return (1 if ny < lay.G else 2), cells, (nx, ny)
+            if len(cells) + 1 > max_cells:
+                return -5, [], None
+            x, yl = nx, ny
+            cells.append((x, yl))
+
+
+def _walk_worker(rank, world, port, k, S, start, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cls, u = _problem()
+    H, W = cls.shape
+    lay = SlabLayout(W, H, world, rank, k)
+    be = OracleSlabBackend(lay, cls, u)
+    ex = DistExchanger()
+    SlabRelaxer(be, lay, ex).relax(S)
+    code, mine, total = sharded_walk(be, lay, ex, start, 4 * W * H)
+    segs = [None] * world
+    dist.all_gather_object(segs, [(c, np.asarray(sg).tolist()) for c, sg in mine])
+    if rank == 0:
+        parts = sorted([p for r in segs for p in r], key=lambda t: t[0])
+        cells = [xy for _, sg in parts for xy in sg]
+        out.put((code, total, cells))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k", [(2, 2), (3, 4)])
+def test_sharded_walk_gloo_equals_single_grid(world, k):
+    import oracle
+    S = 3000
+    start = (3, 58)  # bottom slab; the goal (35, 20) lies in the top one
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_walk_worker, args=(r, world, port, k, S, start, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    code, total, cells = q.get(timeout=180)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    cls, u = _problem()
+    oracle.relax_f32(cls, u, S, S, 0.0)
+    st, ref = oracle.walk(cls, u, start, 4 * cls.size)
+    assert st == oracle.OK and code == WALK_GOAL
+    assert total == len(ref) and np.array_equal(np.asarray(cells), ref)
+    rows = {slab_rows(cls.shape[0], world, r) for r in range(world)}
+    assert len({next(i for i, (a, b) in enumerate(sorted(rows)) if a <= y < b) for _, y in ref}) > 1  # crosses slabs
 
 
 def _worker(rank, world, port, k, S, check_every, tol, out):
