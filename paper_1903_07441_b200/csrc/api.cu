@@ -730,14 +730,13 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     CK(dev_alloc(&c->d_dir, cells));
     CK(cudaMemsetAsync(c->mask, 0, B * c->H * c->W, c->stream));
     CK(cudaMemsetAsync(c->d_meta, 0, B * sizeof(PathMeta), c->stream));
-    static bool preloaded = false;  // eager module loading (process-wide, once)
-    if (!preloaded) {
+    static unsigned long long preloaded = 0;  // eager module loading, once per device
+    if (first_on_device(preloaded)) {
         preload_relax_kernels();
         preload_stamp_kernels();
         preload_path_kernels();
         preload_track_kernels();
         preload_sim_kernels();
-        preloaded = true;
     }
     CK(launch_init_field(c->u[0], c->P, c->sstride, c->W, c->H, c->B, c->stream));
     CK(launch_init_field(c->u[1], c->P, c->sstride, c->W, c->H, c->B, c->stream));

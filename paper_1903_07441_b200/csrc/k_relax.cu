@@ -438,10 +438,9 @@ static cudaError_t launch_T(const CUtensorMap& m0, const CUtensorMap& m1, const 
     const int tasks = a.n_strips * nseg;
     dim3 grid((tasks + kWarpsPerCta - 1) / kWarpsPerCta, B);
     const size_t smem = (size_t)kWarpsPerCta * kStages * (2 * T + 2) * kStripW * 4 + kWarpsPerCta * kStages * sizeof(uint64_t);
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr_mask = 0;
+    if (first_on_device(attr_mask)) {
         cudaFuncSetAttribute(k_rb_tblock<T, QOFF, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     cudaError_t e = launch_pdl(k_rb_tblock<T, QOFF, RESID>, grid, dim3(kWarpsPerCta * 32), smem, st, m0, m1, a);
     if (e != cudaSuccess) return e;

@@ -388,13 +388,11 @@ __global__ void __launch_bounds__(1024) k_trk_compact(TrackArgs t) {
 }
 
 cudaError_t launch_track_step(const TrackArgs& t, int nreq, int max_n, int max_m, int* n_launch, cudaStream_t st) {
-    static bool init = false;
+    static unsigned long long init_mask = 0;
     const size_t smem = kSmemPairs * sizeof(ulonglong2) + ((t.cap + 31) / 32 + (t.mcap + 31) / 32) * sizeof(unsigned);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    if (!init) {
+    if (first_on_device(init_mask))
         cudaFuncSetAttribute(k_trk_assoc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        init = true;
-    }
     const int nm = std::max(std::max(max_n, max_m), 1);
     k_trk_predict<<<dim3((nm + 127) / 128, nreq), 128, 0, st>>>(t);
     const int tiles = ((max_n + kPairTile - 1) / kPairTile) * ((max_m + kPairTile - 1) / kPairTile);

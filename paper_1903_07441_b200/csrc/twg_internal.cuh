@@ -142,6 +142,17 @@ __device__ __forceinline__ void pdl_enter() {
     pdl_trigger();
 }
 
+// True the first time it is called for the current device (per-device one-time set-up of kernel
+// attributes and module loading; a process may hold contexts on several devices).
+inline bool first_on_device(unsigned long long& mask) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+}
+
 __device__ __forceinline__ bool is_free(float v) { return __float_as_int(v) < 0; }
 
 }  // namespace twg
