@@ -19,10 +19,11 @@
  * u = 1 - phi (C3), so goal u = 1, obstacle u = 0, free init 0.5.
  *
  * Parity-pinned functions: see the header of each function; the pins live in
- * tests/test_oracle_pins.py.  Parity unpinned (defined only by the algorithm
- * as written here): the exact smoothed path on general scenes (orc_band, only
- * its properties are pinned), the warm-start trajectory over many ticks
- * (orc_init_u32 warm branch), and the next-waypoint choice (orc_next_waypoint).
+ * tests/test_oracle_pins*.py (P1-P26).  Parity unpinned (defined only by the
+ * algorithm as written here): the exact smoothed path on general scenes
+ * (orc_band: one hand-computed step and its properties are pinned) and the
+ * warm-start trajectory over many ticks (the warm initialisation itself and
+ * the next-waypoint choice are pinned by hand, P25-P26).
  */
 #include <math.h>
 #include <stdint.h>

@@ -261,3 +261,34 @@ def test_p24_lex_spectral_radius(orc):
     u = np.full((N, N), 0.5, np.float32)
     res = [orc.relax_lex_f32(cls, u, 1)[1] for _ in range(200)]
     assert abs(res[-1] / res[-2] - math.cos(math.pi / (N + 1)) ** 2) < 2e-3
+
+
+# --------------------------------------------------------------------- P25 (O8 resample / next waypoint)
+def test_p25_resample_and_next_waypoint_by_hand(orc):
+    # C15: a segment of length l becomes ceil(max(l, 1)) equal sub-steps, the last waypoint appended
+    w = np.array([[0.5, 0.5], [3.0, 0.5], [3.0, 1.0]], np.float32)
+    pts, cnt = orc.resample(w)
+    # segment 1: l = 2.5 -> 3 sub-steps of 5/6; segment 2: l = 0.5 -> 1 sub-step; + last
+    exp = [[0.5, 0.5], [0.5 + 2.5 / 3, 0.5], [0.5 + 5.0 / 3, 0.5], [3.0, 0.5], [3.0, 1.0]]
+    assert cnt == 5 and np.allclose(pts, exp, atol=1e-6)
+    # a9: the first resampled point >= 1 cell from the first one: (0.5 + 5/3, 0.5) at distance 1.67
+    k, nx, ny = orc.next_waypoint(pts)
+    assert k == 2 and abs(nx - (0.5 + 5.0 / 3)) < 1e-6 and ny == 0.5
+    # all within 1 cell: the last point (the goal)
+    k, nx, ny = orc.next_waypoint(np.array([[0.5, 0.5], [1.0, 0.5], [1.2, 0.9]], np.float32))
+    assert (nx, ny) == (np.float32(1.2), np.float32(0.9))
+    # exactly 1 cell away counts (>= 1)
+    k, nx, ny = orc.next_waypoint(np.array([[0.5, 0.5], [1.0, 0.5], [1.5, 0.5], [9.5, 0.5]], np.float32))
+    assert k == 2 and (nx, ny) == (1.5, 0.5)
+
+
+# --------------------------------------------------------------------- P26 (C7 warm start)
+def test_p26_warm_init_by_hand(orc):
+    # C7: free cells keep the previous value, including cells fixed last tick and free now;
+    # fixed cells take their class value (goal 1, obstacle 0)
+    prev = np.array([[0.375, 0.0, 1.0], [0.75, 0.25, 0.125]], np.float32)
+    cls = np.array([[0, 0, 0], [1, 2, 0]], np.uint8)   # the old obstacle (0,1) and goal (0,2) are free now
+    u = orc.init_u32(cls, prev)
+    assert u.tolist() == [[0.375, 0.0, 1.0], [0.0, 1.0, 0.125]]
+    # cold: free 0.5
+    assert orc.init_u32(cls).tolist() == [[0.5, 0.5, 0.5], [0.0, 1.0, 0.5]]
