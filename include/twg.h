@@ -215,7 +215,7 @@ typedef struct {
  * stream).  Allocates 2 ping-pong fields of height x pitch fp32 per scenario
  * (pitch = width rounded up to 32) plus a uint8 static mask.  Every field
  * starts as all-free cold (u = 0.5) with no goal.
- * Errors: INVALID_ARG (sizes <= 0, cell_size <= 0), CUDA, NO_MEMORY. */
+ * Errors: INVALID_ARG (sizes <= 0, cell_size <= 0, batch > 65535), CUDA, NO_MEMORY. */
 TWG_API twg_status twg_create(const twg_grid_desc* desc, int32_t device, void* cuda_stream, twg_ctx** out);
 
 /* Release all device memory of the context.  NULL is a no-op. */

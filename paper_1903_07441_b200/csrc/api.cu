@@ -679,6 +679,8 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     *out = nullptr;
     if (d->width <= 0 || d->height <= 0 || d->batch <= 0 || !(d->cell_size > 0.0))
         return fail(nullptr, TWG_E_INVALID_ARG, "width, height, batch > 0 and cell_size > 0 required");
+    if (d->batch > 65535 || d->width >= (1 << 24) || d->height >= (1 << 24))
+        return fail(nullptr, TWG_E_INVALID_ARG, "batch <= 65535 (one grid dimension per scenario) and sides < 2^24");
     if (d->ghost_rows < 0 || 2 * d->ghost_rows >= d->height)
         return fail(nullptr, TWG_E_INVALID_ARG, "0 <= ghost_rows < height / 2 required");
     cudaError_t e = cudaSetDevice(device);

@@ -49,3 +49,14 @@ def test_create_without_gpu_fails_cleanly():
         pass
     with pytest.raises(twg.TwgError):
         twg.Planner(8, 8)
+
+
+def test_create_validates_arguments_before_touching_a_device():
+    import pytest
+    from paper_1903_07441_b200 import twg
+    for kw in (dict(width=0, height=8), dict(width=8, height=8, batch=0), dict(width=8, height=8, batch=70000),
+               dict(width=8, height=8, cell_size=0.0), dict(width=8, height=8, ghost_rows=4)):
+        w, h = kw.pop("width"), kw.pop("height")
+        with pytest.raises(twg.TwgError) as e:
+            twg.Planner(w, h, **kw)
+        assert e.value.status == twg.E_INVALID_ARG
