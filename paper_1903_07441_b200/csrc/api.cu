@@ -1,677 +1,17 @@
-// api.cu -- the C ABI of include/twg.h: validation, host-side trig, H2D/D2H, buffer
-// management and kernel orchestration.  Every step of the hot path runs in the
-// kernels of k_stamp.cu (a1-a3), k_relax.cu (a4-a6) and k_path.cu (a7-a9).
-#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
-
+// api.cu -- the core entry points of include/twg.h (context, rows a1-a9, field access, accounting).
+// Helpers and the a1-a9 orchestration are in host_core.cu; the 8(f) rows in api_track.cu (f1),
+// api_sim.cu (f2) and api_extra.cu (f3, slab walk).
 #include <algorithm>
 #include <cmath>
-#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
 
-#include "twg_kernels.cuh"
+#include "api_host.cuh"
 
 using namespace twg;
+using namespace twg::host;
 
-namespace {
-
-std::string g_create_err;
-
-twg_status fail(twg_ctx* c, twg_status st, const std::string& msg) {
-    if (c) c->err = msg;
-    else g_create_err = msg;
-    return st;
-}
-
-#define TWG_CUDA(ctx, expr)                                                                                 \
-    do {                                                                                                    \
-        cudaError_t e_ = (expr);                                                                            \
-        if (e_ != cudaSuccess)                                                                              \
-            return fail(ctx, e_ == cudaErrorMemoryAllocation ? TWG_E_NO_MEMORY : TWG_E_CUDA,                \
-                        std::string(#expr) + ": " + cudaGetErrorString(e_));                                \
-    } while (0)
-
-bool is_device_ptr(const void* p) {
-    if (p == nullptr) return false;
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-// 3D map {W, H, B} over one ping-pong buffer; box {128, rows, 1}; OOB -> zero fill.
-bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P, int rows) {
-    auto enc = get_encode();
-    if (!enc) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
-    cuuint64_t strides[2] = {(cuuint64_t)(P * 4), (cuuint64_t)(P * 4 * (int64_t)H)};
-    cuuint32_t box[3] = {(cuuint32_t)kStripW, (cuuint32_t)rows, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-// The index matrix as a 2D {P, H * B} uint16 tensor with box {256, 176}: one box lands in shared
-// memory as 176 rows of 256 contiguous descriptors (k_walk windows, row pitch 256).
-bool make_idx_map(CUtensorMap* m, uint16_t* base, int H, int B, int64_t P) {
-    auto enc = get_encode();
-    if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)H * (cuuint64_t)B};
-    cuuint64_t strides[1] = {(cuuint64_t)P * 2};
-    cuuint32_t box[2] = {256, 176};  // may exceed P: out-of-range columns are zero-filled
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-template <class T>
-cudaError_t dev_alloc(T** p, size_t n) {
-    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T));
-}
-
-// Pinned host staging ring.  Regions are handed out in order; when the ring wraps
-// (or must grow) the stream is synchronised first, so a region is never rewritten
-// while an earlier asynchronous copy may still read it.
-cudaError_t stage_alloc(twg_ctx* c, size_t bytes, void** out) {
-    bytes = (bytes + 255) & ~size_t(255);
-    if (bytes > c->h_stage_bytes) {
-        cudaError_t e = cudaStreamSynchronize(c->stream);
-        if (e != cudaSuccess) return e;
-        if (c->h_stage) cudaFreeHost(c->h_stage);
-        c->h_stage = nullptr;
-        c->h_stage_bytes = 0;
-        const size_t nb = std::max<size_t>(bytes, size_t(8) << 20);
-        e = cudaMallocHost(&c->h_stage, nb);
-        if (e != cudaSuccess) return e;
-        c->h_stage_bytes = nb;
-        c->stage_off = 0;
-    } else if (c->stage_off + bytes > c->h_stage_bytes) {
-        cudaError_t e = cudaStreamSynchronize(c->stream);
-        if (e != cudaSuccess) return e;
-        c->stage_off = 0;
-    }
-    *out = static_cast<char*>(c->h_stage) + c->stage_off;
-    c->stage_off += bytes;
-    return cudaSuccess;
-}
-
-// Grow the per-scenario track arrays to `cap` entries, keeping their contents.
-twg_status ensure_track_cap(twg_ctx* c, int cap) {
-    if (cap <= c->track_cap) return TWG_OK;
-    int nc = std::max(cap, std::max(2 * c->track_cap, 64));
-    const size_t B = c->B;
-    twg_track* t0;
-    int *t1, *t2;
-    double* t3;
-    int4* t4;
-    int* t5;
-    TWG_CUDA(c, dev_alloc(&t0, B * nc));
-    TWG_CUDA(c, dev_alloc(&t5, B * nc));
-    TWG_CUDA(c, dev_alloc(&t1, B * nc));
-    TWG_CUDA(c, dev_alloc(&t2, B * nc));
-    TWG_CUDA(c, dev_alloc(&t3, B * nc * 3));
-    TWG_CUDA(c, dev_alloc(&t4, B * nc));
-    if (c->track_cap > 0) {
-        const int oc = c->track_cap;
-        TWG_CUDA(c, cudaMemcpy2DAsync(t0, nc * sizeof(twg_track), c->d_tracks, oc * sizeof(twg_track),
-                                      oc * sizeof(twg_track), B, cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaMemcpy2DAsync(t1, nc * sizeof(int), c->d_t, oc * sizeof(int), oc * sizeof(int), B,
-                                      cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaMemcpy2DAsync(t2, nc * sizeof(int), c->d_j, oc * sizeof(int), oc * sizeof(int), B,
-                                      cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaMemcpy2DAsync(t3, nc * 3 * sizeof(double), c->d_pred, oc * 3 * sizeof(double),
-                                      oc * 3 * sizeof(double), B, cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaMemcpy2DAsync(t4, nc * sizeof(int4), c->d_boxes, oc * sizeof(int4), oc * sizeof(int4), B,
-                                      cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaMemcpy2DAsync(t5, nc * sizeof(int), c->d_missed, oc * sizeof(int), oc * sizeof(int), B,
-                                      cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-        cudaFree(c->d_tracks);
-        cudaFree(c->d_t);
-        cudaFree(c->d_j);
-        cudaFree(c->d_pred);
-        cudaFree(c->d_boxes);
-        cudaFree(c->d_missed);
-    }
-    c->d_tracks = t0;
-    c->d_t = t1;
-    c->d_j = t2;
-    c->d_pred = t3;
-    c->d_boxes = t4;
-    c->d_missed = t5;
-    c->track_cap = nc;
-    return TWG_OK;
-}
-
-// Parameter block: [WarpCfgDev | pad to 256 B | ScenParams x n], so one copy uploads both.
-constexpr size_t kParamOff = 256;
-static_assert(sizeof(WarpCfgDev) <= kParamOff, "warp cfg does not fit the parameter block header");
-twg_status ensure_params(twg_ctx* c, int n) {
-    if (n <= c->params_cap && c->d_param_block) return TWG_OK;
-    if (c->d_param_block) cudaFree(c->d_param_block);
-    c->d_param_block = nullptr;
-    c->d_params = nullptr;
-    c->d_wcfg = nullptr;
-    const int nc = std::max(n, 1);
-    TWG_CUDA(c, dev_alloc(&c->d_param_block, kParamOff + (size_t)nc * sizeof(ScenParams)));
-    c->d_wcfg = reinterpret_cast<WarpCfgDev*>(c->d_param_block);
-    c->d_params = reinterpret_cast<ScenParams*>(c->d_param_block + kParamOff);
-    c->params_cap = nc;
-    return TWG_OK;
-}
-
-twg_status ensure_path_cap(twg_ctx* c, int max_len, int max_smooth) {
-    const size_t B = c->B;
-    if (max_len > c->path_len_cap) {
-        int nc = std::max(max_len, 256);
-        if (c->d_cells) cudaFree(c->d_cells);
-        if (c->d_wp) cudaFree(c->d_wp);
-        c->d_cells = nullptr;
-        c->d_wp = nullptr;
-        TWG_CUDA(c, dev_alloc(&c->d_cells, B * nc));
-        TWG_CUDA(c, dev_alloc(&c->d_wp, B * nc));
-        c->path_len_cap = nc;
-    }
-    if (max_smooth > c->smooth_cap) {
-        int nc = std::max(max_smooth, 256);
-        if (c->d_smooth) cudaFree(c->d_smooth);
-        c->d_smooth = nullptr;
-        TWG_CUDA(c, dev_alloc(&c->d_smooth, B * nc));
-        c->smooth_cap = nc;
-    }
-    return TWG_OK;
-}
-
-twg_status check_ctx(twg_ctx* c) {
-    if (!c) return TWG_E_INVALID_ARG;
-    cudaError_t e = cudaSetDevice(c->device);
-    if (e != cudaSuccess) return fail(c, TWG_E_CUDA, cudaGetErrorString(e));
-    return TWG_OK;
-}
-
-// One scenario's encode request.
-struct EncodeReq {
-    int b;
-    twg_robot robot;
-    int gx, gy;
-    int n;
-    int64_t track_off;  // offset into the caller's track array
-};
-
-// Host validation -> robot cell.
-twg_status validate(twg_ctx* c, const EncodeReq& r, int* rcx, int* rcy) {
-    const bool slab = c->ghost > 0;  // goal and robot may belong to another slab
-    const bool g_in = r.gx >= 0 && r.gy >= 0 && r.gx < c->W && r.gy < c->H;
-    if (!g_in && !(slab && r.gx >= 0 && r.gx < c->W))
-        return fail(c, TWG_E_OUT_OF_BOUNDS, "goal cell outside the grid");
-    const uint8_t* m = c->hmask.data() + (size_t)r.b * c->H * c->W;
-    if (g_in && m[(size_t)r.gy * c->W + r.gx]) return fail(c, TWG_E_OVERLAPPING_CLASSES, "goal cell on a static wall");
-    const double fx = std::floor((r.robot.x - c->ox) / c->cs), fy = std::floor((r.robot.y - c->oy) / c->cs);
-    const bool r_in = fx >= 0.0 && fy >= 0.0 && fx < (double)c->W && fy < (double)c->H;
-    if (!r_in && !slab) return fail(c, TWG_E_OUT_OF_BOUNDS, "robot cell outside the grid");
-    *rcx = r_in ? (int)fx : -1;
-    *rcy = r_in ? (int)fy : -1;
-    if (r_in && m[(size_t)*rcy * c->W + *rcx]) return fail(c, TWG_E_INVALID_START, "robot cell on a static wall");
-    if (r.n < 0) return fail(c, TWG_E_INVALID_ARG, "negative track count");
-    return TWG_OK;
-}
-
-// Rows a1-a3 for a list of scenarios.  tracks: concatenated per request (host or device).
-// resident: use the tracker tables (row f1) already in d_tracks instead of caller tracks.
-twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_track* tracks, const twg_warp_cfg* wc,
-                  int warm_req, bool resident = false) {
-    if (!wc) return fail(c, TWG_E_INVALID_ARG, "null warp cfg");
-    if ((wc->horizon_mode != 0 && wc->horizon_mode != 1) || (wc->footprint_mode != 0 && wc->footprint_mode != 1))
-        return fail(c, TWG_E_INVALID_ARG, "horizon_mode / footprint_mode must be 0 or 1");
-    const int ns = (int)reqs.size();
-    std::vector<ScenParams> ps(ns);
-    int max_n = 0, max_prev = 0, any_cold = 0;
-    int64_t total = 0;
-    for (int k = 0; k < ns; ++k) {
-        const EncodeReq& r = reqs[k];
-        int rcx, rcy;
-        twg_status st = validate(c, r, &rcx, &rcy);
-        if (st != TWG_OK) return st;
-        twg_ctx::Scen& sc = c->scen[r.b];
-        ScenParams& p = ps[k];
-        p.xr = r.robot.x;
-        p.yr = r.robot.y;
-        p.c = std::cos(r.robot.theta);  // host libm (C25)
-        p.s = std::sin(r.robot.theta);
-        p.speed = r.robot.speed;
-        p.b = r.b;
-        p.gx = r.gx;
-        p.gy = r.gy;
-        p.rcx = rcx;
-        p.rcy = rcy;
-        const bool warm = warm_req && sc.encoded && !sc.static_dirty;
-        p.warm = warm ? 1 : 0;
-        p.old_gx = warm ? sc.gx : -1;
-        p.old_gy = warm ? sc.gy : -1;
-        p.cur = c->cur[r.b];
-        p.n_tracks = r.n;
-        p.n_prev_boxes = warm ? sc.n_boxes : 0;
-        max_n = std::max(max_n, r.n);
-        max_prev = std::max(max_prev, p.n_prev_boxes);
-        any_cold |= !warm;
-        total += r.n;
-    }
-    twg_status st = ensure_track_cap(c, std::max(max_n, 1));
-    if (st != TWG_OK) return st;
-    st = ensure_params(c, ns);
-    if (st != TWG_OK) return st;
-    // tracks -> [B][cap]: one contiguous copy (device input: in place; host input: through the pinned
-    // staging ring and one H2D copy) and one scatter kernel for every scenario of the call
-    if (total > 0 && !resident) {
-        const twg_track* src = tracks;
-        if (!is_device_ptr(tracks)) {
-            if (c->track_tmp_cap < total) {
-                if (c->d_track_tmp) cudaFree(c->d_track_tmp);
-                c->d_track_tmp = nullptr;
-                TWG_CUDA(c, dev_alloc(&c->d_track_tmp, (size_t)total));
-                c->track_tmp_cap = total;
-            }
-            twg_track* ht = nullptr;
-            TWG_CUDA(c, stage_alloc(c, (size_t)total * sizeof(twg_track), reinterpret_cast<void**>(&ht)));
-            int64_t first = reqs[0].track_off;
-            std::memcpy(ht, tracks + first, (size_t)total * sizeof(twg_track));
-            TWG_CUDA(c, cudaMemcpyAsync(c->d_track_tmp, ht, (size_t)total * sizeof(twg_track), cudaMemcpyHostToDevice,
-                                        c->stream));
-            src = c->d_track_tmp - first;  // offsets below are relative to the caller's array
-        }
-        std::vector<int> off(ns + 1), sb(ns);
-        for (int k = 0; k < ns; ++k) {
-            off[k] = (int)reqs[k].track_off;
-            sb[k] = reqs[k].b;
-        }
-        off[ns] = (int)(reqs[ns - 1].track_off + reqs[ns - 1].n);
-        if (c->track_off_cap < 2 * ns + 1) {
-            if (c->d_track_off) cudaFree(c->d_track_off);
-            c->d_track_off = nullptr;
-            TWG_CUDA(c, dev_alloc(&c->d_track_off, 2 * ns + 1));
-            c->track_off_cap = 2 * ns + 1;
-        }
-        int* hs = nullptr;
-        TWG_CUDA(c, stage_alloc(c, (2 * ns + 1) * sizeof(int), reinterpret_cast<void**>(&hs)));
-        std::memcpy(hs, off.data(), (ns + 1) * sizeof(int));
-        std::memcpy(hs + ns + 1, sb.data(), ns * sizeof(int));
-        TWG_CUDA(c, cudaMemcpyAsync(c->d_track_off, hs, (2 * ns + 1) * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        TWG_CUDA(c, launch_scatter_tracks(src, c->d_track_off, ns, c->d_track_off + ns + 1, c->d_tracks, c->d_missed,
-                                          c->track_cap, c->stream));
-        c->launches += 1;
-    }
-    // per-scenario params + cfg (pinned staging, one copy each)
-    WarpCfgDev w;
-    w.dt = wc->dt;
-    std::memcpy(w.Q, wc->Q, sizeof(w.Q));
-    w.w = wc->warp_spacing;
-    w.eps_v = wc->eps_v;
-    w.rs = wc->safety_radius;
-    w.hmax = wc->horizon_max;
-    w.hmode = wc->horizon_mode;
-    w.fmode = wc->footprint_mode;
-    // warp cfg + per-scenario params: one copy into the parameter block (warning flags are cleared
-    // by k_goal_reset, which runs before the stamping kernels that set them)
-    const size_t pbytes = kParamOff + ns * sizeof(ScenParams);
-    char* hs = nullptr;
-    TWG_CUDA(c, stage_alloc(c, pbytes, reinterpret_cast<void**>(&hs)));
-    std::memcpy(hs, &w, sizeof(w));
-    std::memcpy(hs + kParamOff, ps.data(), ns * sizeof(ScenParams));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_param_block, hs, pbytes, cudaMemcpyHostToDevice, c->stream));
-    EncodeArgs e;
-    e.u0 = c->u[0];
-    e.u1 = c->u[1];
-    e.P = c->P;
-    e.sstride = c->sstride;
-    e.W = c->W;
-    e.H = c->H;
-    e.mask = c->mask;
-    e.params = c->d_params;
-    e.nscen = ns;
-    e.wcfg = c->d_wcfg;
-    e.tracks = c->d_tracks;
-    e.cap = c->track_cap;
-    e.t_out = c->d_t;
-    e.j_out = c->d_j;
-    e.pred = c->d_pred;
-    e.boxes = c->d_boxes;
-    e.flags = c->d_flags;
-    e.cs = c->cs;
-    e.ox = c->ox;
-    e.oy = c->oy;
-    int nl = 0;
-    TWG_CUDA(c, launch_encode(e, max_prev, max_n, any_cold, &nl, c->stream));
-    c->launches += nl;
-    // host-side bookkeeping for the next warm encode
-    for (int k = 0; k < ns; ++k) {
-        twg_ctx::Scen& sc = c->scen[reqs[k].b];
-        sc.gx = ps[k].gx;
-        sc.gy = ps[k].gy;
-        sc.rcx = ps[k].rcx;
-        sc.rcy = ps[k].rcy;
-        sc.n_tracks = reqs[k].n;
-        if (!resident) sc.trk_n = reqs[k].n;
-        sc.n_boxes = reqs[k].n;
-        sc.encoded = true;
-        sc.static_dirty = false;
-    }
-    return TWG_OK;
-}
-
-// Output rows per warp (hseg).  hseg + 4T is a multiple of NW = 2T + 2 (the kernel streams whole
-// NW-row blocks, so any other value pays for padded rows) and even (the colour parity of the first
-// row is a compile-time constant).  Among those, pick the one minimising the load model measured on
-// B200: a launch takes ~ (CTAs on the busiest SM) x (hseg + 4T) /
-// min(CTAs per SM, 2) -- throughput saturates at two 4-warp CTAs per SM.
-int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows, int n_sm) {
-    const int NW = 2 * T + 2;
-    if (cfg_rows > 0) {
-        int h = std::min(cfg_rows, H);
-        h = (h + 1) & ~1;
-        return std::max(h, 2);
-    }
-    int best_h = 2;
-    double best = 1e300;
-    for (int k = 1; k <= 256; ++k) {
-        const int h = k * NW - 4 * T;
-        if (h < 2) continue;
-        const int hh = std::min(h, (H + 1) & ~1);
-        const long long segs = (H + hh - 1) / hh;
-        const long long ctas = (segs * n_strips * nscen + kWarpsPerCta - 1) / kWarpsPerCta;
-        const long long per_sm = (ctas + n_sm - 1) / n_sm;
-        const double cost = (double)per_sm * (hh + 4 * T) / (double)std::min<long long>(per_sm, 2);
-        if (cost < best * 0.999) {
-            best = cost;
-            best_h = hh;
-        }
-        if (h >= H) break;
-    }
-    return std::max(best_h, 2);
-}
-
-// Rows a4-a6 for the scenarios whose participation flag is set.
-// Task lists and counters of the lexicographic mode: 32 x 32 tiles, tasks (sweep s, tile (i, j)) of
-// one launch of `sweeps` sweeps ordered by wavefront time i + j + 2 s, then s, then j.  Every
-// dependency of a task has a smaller time, so the order is topological.  Lists are cached per
-// launch length (a relaxation uses at most two: kLexMaxSweeps and its remainder).
-constexpr int kLexMaxSweeps = 64;  // sweeps per persistent launch
-int2* lex_tasks(twg_ctx* c, int sweeps) {
-    for (auto& e : c->lex_lists)
-        if (e.first == sweeps) return e.second;
-    const int tx = c->lex_tx, ty = c->lex_ty;
-    std::vector<int2> ord;
-    ord.reserve((size_t)tx * ty * sweeps);
-    const int dmax = tx + ty - 2;
-    for (int tau = 0; tau <= dmax + 2 * (sweeps - 1); ++tau)
-        for (int s = 0; s < sweeps; ++s) {
-            const int d = tau - 2 * s;
-            if (d < 0 || d > dmax) continue;
-            for (int j = 0; j < ty; ++j) {
-                const int i = d - j;
-                if (i >= 0 && i < tx) ord.push_back(make_int2(i | (s << 16), j));
-            }
-        }
-    int2* d = nullptr;
-    if (dev_alloc(&d, ord.size()) != cudaSuccess) return nullptr;
-    if (cudaMemcpy(d, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess) {
-        cudaFree(d);
-        return nullptr;
-    }
-    if (c->lex_lists.size() >= 4) {  // keep a handful
-        cudaFree(c->lex_lists.front().second);
-        c->lex_lists.erase(c->lex_lists.begin());
-    }
-    c->lex_lists.emplace_back(sweeps, d);
-    return d;
-}
-
-twg_status ensure_lex(twg_ctx* c) {
-    if (c->d_lex_tdone) return TWG_OK;
-    c->lex_tx = (c->W + 31) / 32;
-    c->lex_ty = (c->H + 31) / 32;
-    TWG_CUDA(c, dev_alloc(&c->d_lex_tdone, (size_t)c->B * c->lex_tx * c->lex_ty));
-    TWG_CUDA(c, dev_alloc(&c->d_lex_task, 1));
-    return TWG_OK;
-}
-
-twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& part, int* sweeps_done,
-                 float* residual) {
-    if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null relax cfg");
-    const int maxs = cfg->max_sweeps;
-    if (maxs < 0 || cfg->check_every < 0) return fail(c, TWG_E_INVALID_ARG, "negative sweep counts");
-    if (cfg->mode < 0 || cfg->mode > 2) return fail(c, TWG_E_INVALID_ARG, "relax mode must be 0, 1 or 2");
-    const bool jacobi = cfg->mode == 1;
-    const bool lex = cfg->mode == 2;
-    if (lex && c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "lexicographic mode is not available on a row slab");
-    if (lex) {
-        twg_status ls = ensure_lex(c);
-        if (ls != TWG_OK) return ls;
-    }
-    const int B = c->B;
-    int T = cfg->temporal_depth > 0 ? std::min(cfg->temporal_depth, kMaxT) : 6;
-    const float tol = cfg->tol;
-    int check = (tol > 0.0f && cfg->check_every > 0) ? cfg->check_every : std::max(maxs, 1);
-    const int sync_every = cfg->sync_every > 0 ? cfg->sync_every : 64;
-    // control arrays [done | cur | sweeps | where | res bits | res]: one copy (done = !participating,
-    // where = -1: not (yet) finished)
-    int* hs = nullptr;
-    TWG_CUDA(c, stage_alloc(c, 6 * B * sizeof(int), reinterpret_cast<void**>(&hs)));
-    for (int b = 0; b < B; ++b) {
-        hs[b] = part[b] ? 0 : 1;
-        hs[B + b] = c->cur[b];
-        hs[2 * B + b] = 0;
-        hs[3 * B + b] = -1;
-        hs[4 * B + b] = 0;
-        hs[5 * B + b] = 0;  // +0.0f
-    }
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_ctl, hs, 6 * B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    if (lex)
-        TWG_CUDA(c, cudaMemsetAsync(c->d_lex_tdone, 0, (size_t)B * c->lex_tx * c->lex_ty * sizeof(int), c->stream));
-    int nscen = 0;
-    for (int b = 0; b < B; ++b) nscen += part[b] ? 1 : 0;
-
-    int lp = 0;  // launches so far (parity)
-    if (maxs > 0) {
-        RelaxArgs a;
-        a.u0 = c->u[0];
-        a.u1 = c->u[1];
-        a.cur = c->d_cur;
-        a.P = c->P;
-        a.sstride = c->sstride;
-        a.W = c->W;
-        a.H = c->H;
-        a.done = c->d_done;
-        a.res = c->d_res_bits;
-        a.res_r0 = c->ghost;
-        a.res_r1 = c->H - c->ghost;
-        const int qoff = c->row_off & 1;
-        int done_sw = 0, nchunk = 0;
-        int lex_base = 0;  // sweeps finished by earlier lexicographic launches of this call
-        while (done_sw < maxs) {
-            const int chunk = std::min(check, maxs - done_sw);
-            // launches of T sweeps, then the remainder; the last launch accumulates the residual (the
-            // tracking costs the most in the deepest kernel, so a short remainder launch carries it)
-            std::vector<int> plan;
-            if (jacobi) {
-                plan.assign(chunk, 1);
-            } else if (lex) {
-                for (int q = 0; q < chunk / kLexMaxSweeps; ++q) plan.push_back(kLexMaxSweeps);  // persistent launches
-                if (chunk % kLexMaxSweeps) plan.push_back(chunk % kLexMaxSweeps);
-            } else {
-                for (int q = 0; q < chunk / T; ++q) plan.push_back(T);
-                if (chunk % T) plan.push_back(chunk % T);
-            }
-            for (size_t q = 0; q < plan.size(); ++q) {
-                const int t = plan[q];
-                a.n_strips = (c->W + out_cols(t) - 1) / out_cols(t);
-                a.hseg = auto_hseg(t, c->H, a.n_strips, std::max(nscen, 1), cfg->rows_per_warp, c->n_sm);
-                a.seg_begin = 0;
-                a.seg_end = (c->H + a.hseg - 1) / a.hseg;
-                a.lp = lp & 1;
-                cudaEvent_t e0 = nullptr, e1 = nullptr;
-                if (c->prof) {
-                    while ((int)c->ev_pool.size() < c->ev_used + 2) {
-                        cudaEvent_t ev;
-                        TWG_CUDA(c, cudaEventCreate(&ev));
-                        c->ev_pool.push_back(ev);
-                    }
-                    e0 = c->ev_pool[c->ev_used++];
-                    e1 = c->ev_pool[c->ev_used++];
-                    TWG_CUDA(c, cudaEventRecord(e0, c->stream));
-                }
-                if (lex) {
-                    int2* tl = lex_tasks(c, t);
-                    if (!tl) return fail(c, TWG_E_NO_MEMORY, "lexicographic task list");
-                    LexArgs la;
-                    la.u0 = c->u[0];
-                    la.u1 = c->u[1];
-                    la.cur = c->d_cur;
-                    la.P = c->P;
-                    la.sstride = c->sstride;
-                    la.W = c->W;
-                    la.H = c->H;
-                    la.B = B;
-                    la.TX = c->lex_tx;
-                    la.TY = c->lex_ty;
-                    la.ntiles = c->lex_tx * c->lex_ty;
-                    la.tasks = tl;
-                    la.ntasks = t * c->lex_tx * c->lex_ty;
-                    la.sweeps = t;
-                    la.base = lex_base;
-                    lex_base += t;
-                    la.tdone = c->d_lex_tdone;
-                    la.task = c->d_lex_task;
-                    la.done = c->d_done;
-                    la.res = q + 1 == plan.size() ? c->d_res_bits : nullptr;  // the chunk's last sweep only
-                    la.res_r0 = c->ghost;
-                    la.res_r1 = c->H - c->ghost;
-                    TWG_CUDA(c, cudaMemsetAsync(c->d_lex_task, 0, sizeof(unsigned), c->stream));
-                    TWG_CUDA(c, launch_lex(la, c->n_sm, c->stream));
-                } else if (jacobi)
-                    TWG_CUDA(c, launch_jacobi(a, B, q + 1 == plan.size(), c->stream));
-                else
-                    TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0][t], c->tmap[1][t], a, B, qoff, q + 1 == plan.size(),
-                                                 c->stream));
-                if (c->prof) {
-                    TWG_CUDA(c, cudaEventRecord(e1, c->stream));
-                    c->prof_launches += 1;
-                    c->prof_cells += (int64_t)nscen * c->W * c->H * t;
-                }
-                c->launches += 1;
-                if (!lex) ++lp;  // the lexicographic sweep is in place
-            }
-            TWG_CUDA(c, launch_check(B, c->d_done, c->d_sweeps, c->d_res_bits, c->d_res, c->d_where, chunk, check, maxs,
-                                     tol, c->d_cur, lp & 1, c->stream));
-            c->launches += 1;
-            done_sw += chunk;
-            ++nchunk;
-            if (tol > 0.0f && done_sw < maxs && nchunk % sync_every == 0) {
-                int* hd = nullptr;
-                TWG_CUDA(c, stage_alloc(c, B * sizeof(int), reinterpret_cast<void**>(&hd)));
-                TWG_CUDA(c, cudaMemcpyAsync(hd, c->d_done, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-                TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-                bool all = true;
-                for (int b = 0; b < B; ++b) all = all && hd[b];
-                if (all) break;
-            }
-        }
-        if (tol > 0.0f) {  // only an early stop can leave a field in the other buffer
-            TWG_CUDA(c, launch_fixup(c->u[0], c->u[1], c->sstride, B, c->d_where, c->d_cur, lp & 1, c->stream));
-            c->launches += 1;
-        }
-        for (int b = 0; b < B; ++b)
-            if (part[b]) c->cur[b] ^= (lp & 1);
-    }
-    if (sweeps_done || residual) {
-        int* hsw = nullptr;  // [sweeps | where | res bits | res] in one copy
-        TWG_CUDA(c, stage_alloc(c, 4 * B * sizeof(int), reinterpret_cast<void**>(&hsw)));
-        float* hr = reinterpret_cast<float*>(hsw + 3 * B);
-        TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, 4 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-        for (int b = 0; b < B; ++b) {
-            if (sweeps_done) sweeps_done[b] = hsw[b];
-            if (residual) residual[b] = hr[b];
-        }
-    }
-    return TWG_OK;
-}
-
-// Rows a7-a9 for a list of scenarios (path kernels only; results stay on device).
-twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg) {
-    if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null band cfg");
-    if (cfg->max_len < 1 || cfg->max_smooth < 1 || cfg->iterations < 0 || cfg->iterations > 6000)
-        return fail(c, TWG_E_INVALID_ARG, "band cfg: max_len, max_smooth >= 1, 0 <= iterations <= 6000");
-    twg_status st = ensure_path_cap(c, cfg->max_len, cfg->max_smooth);
-    if (st != TWG_OK) return st;
-    const int ns = (int)bs.size();
-    st = ensure_params(c, ns);
-    if (st != TWG_OK) return st;
-    std::vector<ScenParams> ps(ns);
-    for (int k = 0; k < ns; ++k) {
-        const twg_ctx::Scen& sc = c->scen[bs[k]];
-        if (!sc.encoded) return fail(c, TWG_E_INVALID_ARG, "extract_path before set_obstacles");
-        std::memset(&ps[k], 0, sizeof(ScenParams));
-        ps[k].b = bs[k];
-        ps[k].gx = sc.gx;
-        ps[k].gy = sc.gy;
-        ps[k].rcx = sc.rcx;
-        ps[k].rcy = sc.rcy;
-        ps[k].cur = c->cur[bs[k]];
-    }
-    void* hp = nullptr;
-    TWG_CUDA(c, stage_alloc(c, ns * sizeof(ScenParams), &hp));
-    std::memcpy(hp, ps.data(), ns * sizeof(ScenParams));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_params, hp, ns * sizeof(ScenParams), cudaMemcpyHostToDevice, c->stream));
-    PathArgs p;
-    p.u0 = c->u[0];
-    p.u1 = c->u[1];
-    p.P = c->P;
-    p.sstride = c->sstride;
-    p.W = c->W;
-    p.H = c->H;
-    p.params = c->d_params;
-    p.nscen = ns;
-    p.max_len = cfg->max_len;
-    p.max_smooth = cfg->max_smooth;
-    p.iters = cfg->iterations;
-    p.step = cfg->step;
-    p.kt = cfg->k_t;
-    p.cells = c->d_cells;
-    p.wp = c->d_wp;
-    p.smooth = c->d_smooth;
-    p.len_cap = c->path_len_cap;
-    p.smooth_cap = c->smooth_cap;
-    p.meta = c->d_meta;
-    p.idx = c->d_idx;
-    p.dir = c->d_dir;
-    p.win_pitch = 256;  // k_walk window pitch (TMA zero-fills columns beyond the grid)
-    p.istride = c->sstride;
-    p.idx_map = c->idx_map;
-    int nl = 0;
-    TWG_CUDA(c, launch_path(p, &nl, c->stream));
-    c->launches += nl;
-    return TWG_OK;
-}
-
-}  // namespace
 
 // =====================================================================================
 TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stream, twg_ctx** out) {
@@ -1000,551 +340,6 @@ TWG_API twg_status twg_get_warp(twg_ctx* c, int32_t b, int32_t n, int32_t* t, in
     return TWG_OK;
 }
 
-namespace {
-// Row f1 tick for the requests rq (det_off relative to `det`, a device array of (x, y) pairs).
-twg_status track_core(twg_ctx* c, std::vector<TrkReq> rq, const double2* det, const twg_warp_cfg* wc,
-                      const twg_tracker_cfg* cfg, std::vector<int>& n_out) {
-    twg_status st = TWG_OK;
-    const int nreq = (int)rq.size();
-    n_out.clear();
-    if (nreq == 0) return TWG_OK;
-    int max_n = 0, max_m = 0, need_cap = 1;
-    for (const TrkReq& r : rq) {
-        max_n = std::max(max_n, r.n);
-        max_m = std::max(max_m, r.m);
-        need_cap = std::max(need_cap, r.n + r.m);
-    }
-    st = ensure_track_cap(c, need_cap);
-    if (st != TWG_OK) return st;
-    for (int k = 0; k < nreq; ++k)
-        rq[k].limit = cfg->max_tracks > 0 ? std::min(cfg->max_tracks, c->track_cap) : c->track_cap;
-    // scratch: [B][cap] tables, [nreq][mcap] flags, [nreq][pcap] pairs, control words, requests, detections
-    if (c->trk_scratch_cap < c->track_cap) {
-        for (void* p : {(void*)c->d_trk_pred, (void*)c->d_trk_misn, (void*)c->d_trk_match})
-            if (p) cudaFree(p);
-        c->d_trk_pred = nullptr;
-        c->d_trk_misn = c->d_trk_match = nullptr;
-        TWG_CUDA(c, dev_alloc(&c->d_trk_pred, (size_t)c->B * c->track_cap));
-        TWG_CUDA(c, dev_alloc(&c->d_trk_misn, (size_t)c->B * c->track_cap));
-        TWG_CUDA(c, dev_alloc(&c->d_trk_match, (size_t)c->B * c->track_cap));
-        c->trk_scratch_cap = c->track_cap;
-    }
-    int pcap = 4096;
-    while (pcap < 4 * (max_n + max_m)) pcap <<= 1;
-    pcap = std::max(pcap, c->trk_pcap);
-    const int mcap = std::max(max_m, 1);
-    auto alloc_req_scratch = [&](int pc) -> twg_status {
-        if (c->trk_nreq_cap < nreq || c->trk_mcap < mcap) {
-            if (c->d_trk_used) cudaFree(c->d_trk_used);
-            c->d_trk_used = nullptr;
-            TWG_CUDA(c, dev_alloc(&c->d_trk_used, (size_t)std::max(nreq, c->trk_nreq_cap) * std::max(mcap, c->trk_mcap)));
-            c->trk_mcap = std::max(mcap, c->trk_mcap);
-        }
-        if (c->trk_nreq_cap < nreq || c->trk_pcap < pc) {
-            if (c->d_trk_pairs) cudaFree(c->d_trk_pairs);
-            c->d_trk_pairs = nullptr;
-            TWG_CUDA(c, dev_alloc(&c->d_trk_pairs, (size_t)std::max(nreq, c->trk_nreq_cap) * std::max(pc, c->trk_pcap)));
-            c->trk_pcap = std::max(pc, c->trk_pcap);
-        }
-        if (c->trk_nreq_cap < nreq) {
-            if (c->d_trk_ctl) cudaFree(c->d_trk_ctl);
-            if (c->d_trk_req) cudaFree(c->d_trk_req);
-            c->d_trk_ctl = nullptr;
-            c->d_trk_req = nullptr;
-            TWG_CUDA(c, dev_alloc(&c->d_trk_ctl, (size_t)3 * nreq));
-            TWG_CUDA(c, dev_alloc(&c->d_trk_req, (size_t)nreq));
-            c->trk_nreq_cap = nreq;
-        }
-        return TWG_OK;
-    };
-    st = alloc_req_scratch(pcap);
-    if (st != TWG_OK) return st;
-    TrackArgs t;
-    t.trk = c->d_tracks;
-    t.missed = c->d_missed;
-    t.pred = c->d_trk_pred;
-    t.mis_new = c->d_trk_misn;
-    t.match = c->d_trk_match;
-    t.det = det;
-    t.cap = c->track_cap;
-    t.mcap = c->trk_mcap;
-    t.prune_after = cfg->prune_after;
-    std::memcpy(t.Q, wc->Q, sizeof(t.Q));
-    t.dt = wc->dt;
-    t.r2 = cfg->sigma_z * cfg->sigma_z;
-    t.gate2 = cfg->gate * cfg->gate;
-    t.var_pos = cfg->spawn_var_pos;
-    t.var_vel = cfg->spawn_var_vel;
-    std::vector<int> result_n(nreq, 0);
-    int worst = 0;
-    std::vector<TrkReq> todo = rq;
-    std::vector<int> todo_idx(nreq);
-    for (int k = 0; k < nreq; ++k) todo_idx[k] = k;
-    for (int attempt = 0; !todo.empty(); ++attempt) {
-        const int nr = (int)todo.size();
-        int mn = 0, mm = 0;
-        for (const TrkReq& r : todo) {
-            mn = std::max(mn, r.n);
-            mm = std::max(mm, r.m);
-        }
-        void* hq = nullptr;
-        TWG_CUDA(c, stage_alloc(c, nr * sizeof(TrkReq), &hq));
-        std::memcpy(hq, todo.data(), nr * sizeof(TrkReq));
-        TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_req, hq, nr * sizeof(TrkReq), cudaMemcpyHostToDevice, c->stream));
-        TWG_CUDA(c, cudaMemsetAsync(c->d_trk_ctl, 0, 3 * nr * sizeof(int), c->stream));
-        t.req = c->d_trk_req;
-        t.used = c->d_trk_used;
-        t.pairs = c->d_trk_pairs;
-        t.pcap = c->trk_pcap;
-        t.pcount = c->d_trk_ctl;
-        t.flags = c->d_trk_ctl + nr;
-        t.n_out = c->d_trk_ctl + 2 * nr;
-        int nl = 0;
-        TWG_CUDA(c, launch_track_step(t, nr, mn, mm, &nl, c->stream));
-        c->launches += nl;
-        int* hc = nullptr;
-        TWG_CUDA(c, stage_alloc(c, 3 * nr * sizeof(int), reinterpret_cast<void**>(&hc)));
-        TWG_CUDA(c, cudaMemcpyAsync(hc, c->d_trk_ctl, 3 * nr * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-        std::vector<TrkReq> again;
-        std::vector<int> again_idx;
-        int need = 0;
-        for (int q = 0; q < nr; ++q) {
-            const int fl = hc[nr + q];
-            if (fl & kTrkOverflow) {  // more gated pairs than the list holds: grow and redo this scenario
-                again.push_back(todo[q]);
-                again_idx.push_back(todo_idx[q]);
-                need = std::max(need, hc[q]);
-                continue;
-            }
-            result_n[todo_idx[q]] = hc[2 * nr + q];
-            c->scen[todo[q].b].trk_n = hc[2 * nr + q];
-            if (fl & kTrkSingular) worst = std::max(worst, (int)TWG_W_SINGULAR_INNOVATION);
-            if (fl & kTrkTruncated) worst = std::max(worst, (int)TWG_W_TRUNCATED);
-        }
-        if (!again.empty()) {
-            if (attempt > 40) return fail(c, TWG_E_NO_MEMORY, "tracker pair list cannot grow");
-            int pc = c->trk_pcap;
-            while (pc < need) pc <<= 1;
-            st = alloc_req_scratch(pc);
-            if (st != TWG_OK) return st;
-        }
-        todo.swap(again);
-        todo_idx.swap(again_idx);
-    }
-    n_out.assign(result_n.begin(), result_n.end());
-    return (twg_status)worst;
-}
-
-
-}  // namespace
-
-TWG_API twg_status twg_track_update(twg_ctx* c, int32_t b, const double* det_xy, const int32_t* n_det,
-                                    const twg_warp_cfg* wc, const twg_tracker_cfg* cfg, int32_t* n_tracks) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (!n_det || !wc || !cfg || b < -1 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    if (!(cfg->sigma_z >= 0.0) || !(cfg->gate >= 0.0) || !(cfg->spawn_var_pos >= 0.0) || !(cfg->spawn_var_vel >= 0.0) ||
-        cfg->prune_after < 0 || cfg->max_tracks < 0)
-        return fail(c, TWG_E_INVALID_ARG, "tracker cfg: sigma_z, gate, variances >= 0, prune_after, max_tracks >= 0");
-    const int nreq = b < 0 ? c->B : 1;
-    std::vector<TrkReq> rq(nreq);
-    int64_t total = 0;
-    for (int k = 0; k < nreq; ++k) {
-        if (n_det[k] < 0) return fail(c, TWG_E_INVALID_ARG, "negative detection count");
-        rq[k].b = b < 0 ? k : b;
-        rq[k].n = c->scen[rq[k].b].trk_n;
-        rq[k].m = n_det[k];
-        rq[k].det_off = total;
-        total += n_det[k];
-    }
-    if (total > 0 && !det_xy) return fail(c, TWG_E_INVALID_ARG, "null detections");
-    // detections -> device (double2)
-    const double2* det = nullptr;
-    if (total > 0) {
-        if (is_device_ptr(det_xy) && (reinterpret_cast<uintptr_t>(det_xy) & 15) == 0) {
-            det = reinterpret_cast<const double2*>(det_xy);
-        } else {
-            if (c->trk_det_cap < total) {
-                if (c->d_trk_det) cudaFree(c->d_trk_det);
-                c->d_trk_det = nullptr;
-                TWG_CUDA(c, dev_alloc(&c->d_trk_det, (size_t)total));
-                c->trk_det_cap = total;
-            }
-            if (is_device_ptr(det_xy)) {
-                TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_det, det_xy, (size_t)total * sizeof(double2),
-                                            cudaMemcpyDeviceToDevice, c->stream));
-            } else {
-                void* hd = nullptr;
-                TWG_CUDA(c, stage_alloc(c, (size_t)total * sizeof(double2), &hd));
-                std::memcpy(hd, det_xy, (size_t)total * sizeof(double2));
-                TWG_CUDA(c, cudaMemcpyAsync(c->d_trk_det, hd, (size_t)total * sizeof(double2), cudaMemcpyHostToDevice,
-                                            c->stream));
-            }
-            det = c->d_trk_det;
-        }
-    }
-    std::vector<int> nout;
-    st = track_core(c, rq, det, wc, cfg, nout);
-    if (st < 0) return st;
-    if (n_tracks)
-        for (int k = 0; k < nreq; ++k) n_tracks[k] = nout[k];
-    return st;
-}
-
-TWG_API twg_status twg_get_tracks(twg_ctx* c, int32_t b, twg_track* out, int32_t* missed, int32_t cap, int32_t* n) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (b < 0 || b >= c->B || cap < 0) return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    const int nt = c->scen[b].trk_n;
-    if (n) *n = nt;
-    const int k = std::min(cap, nt);
-    if (k > 0) {
-        const int64_t o = (int64_t)b * c->track_cap;
-        if (out)
-            TWG_CUDA(c, cudaMemcpyAsync(out, c->d_tracks + o, k * sizeof(twg_track), cudaMemcpyDefault, c->stream));
-        if (missed)
-            TWG_CUDA(c, cudaMemcpyAsync(missed, c->d_missed + o, k * sizeof(int), cudaMemcpyDefault, c->stream));
-    }
-    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    return TWG_OK;
-}
-
-namespace {
-// Simulator buffers with room for `ocap` obstacles per trial (contents kept when growing).
-twg_status ensure_sim(twg_ctx* c, int ocap) {
-    const size_t B = c->B;
-    if (!c->d_sim_rob) {
-        TWG_CUDA(c, dev_alloc(&c->d_sim_rob, B * 6));
-        TWG_CUDA(c, dev_alloc(&c->d_sim_int, B * 2));
-        TWG_CUDA(c, dev_alloc(&c->d_sim_goal, B * 2));
-        TWG_CUDA(c, dev_alloc(&c->d_sim_nobs, B));
-        TWG_CUDA(c, dev_alloc(&c->d_sim_hist, B * 36));
-        c->sim_rob.assign(B * 6, 0.0);
-        c->sim_ticks.assign(B, 0);
-        c->sim_status.assign(B, 4);
-        c->sim_nobs.assign(B, 0);
-        std::vector<int> init(2 * B, 0);
-        for (size_t b = 0; b < B; ++b) init[B + b] = 4;  // idle
-        TWG_CUDA(c, cudaMemcpy(c->d_sim_int, init.data(), 2 * B * sizeof(int), cudaMemcpyHostToDevice));
-        TWG_CUDA(c, cudaMemset(c->d_sim_nobs, 0, B * sizeof(int)));
-    }
-    if (ocap <= c->sim_ocap) return TWG_OK;
-    const int nc = std::max(ocap, std::max(2 * c->sim_ocap, 16));
-    double *o, *oo, *sp;
-    double2* dt;
-    TWG_CUDA(c, dev_alloc(&o, B * nc * 4));
-    TWG_CUDA(c, dev_alloc(&oo, B * nc * 4));
-    TWG_CUDA(c, dev_alloc(&sp, B * nc));
-    TWG_CUDA(c, dev_alloc(&dt, B * nc));
-    if (c->sim_ocap > 0) {
-        const int oc = c->sim_ocap;
-        TWG_CUDA(c, cudaMemcpy2DAsync(o, nc * 4 * sizeof(double), c->d_sim_obs, oc * 4 * sizeof(double),
-                                      oc * 4 * sizeof(double), B, cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaMemcpy2DAsync(sp, nc * sizeof(double), c->d_sim_speed, oc * sizeof(double), oc * sizeof(double),
-                                      B, cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaMemcpy2DAsync(dt, nc * sizeof(double2), c->d_sim_det, oc * sizeof(double2),
-                                      oc * sizeof(double2), B, cudaMemcpyDeviceToDevice, c->stream));
-        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-        cudaFree(c->d_sim_obs);
-        cudaFree(c->d_sim_obs_old);
-        cudaFree(c->d_sim_speed);
-        cudaFree(c->d_sim_det);
-    }
-    c->d_sim_obs = o;
-    c->d_sim_obs_old = oo;
-    c->d_sim_speed = sp;
-    c->d_sim_det = dt;
-    c->sim_ocap = nc;
-    return TWG_OK;
-}
-
-bool sim_cfg_ok(const twg_sim_cfg* f) {
-    return f && f->dt > 0.0 && f->robot_radius >= 0.0 && f->obstacle_radius >= 0.0 && f->goal_radius >= 0.0 &&
-           f->turn_distance >= 0.0 && f->heading_sigma >= 0.0 && f->det_sigma >= 0.0 && f->turn_max >= 0.0 &&
-           f->max_ticks > 0 && f->init_max_sweeps >= 0;
-}
-
-SimArgs sim_args(twg_ctx* c, const twg_sim_cfg* f) {
-    SimArgs a;
-    a.B = c->B;
-    a.W = c->W;
-    a.H = c->H;
-    a.ocap = c->sim_ocap;
-    a.cs = c->cs;
-    a.ox = c->ox;
-    a.oy = c->oy;
-    a.mask = c->mask;
-    a.rob = c->d_sim_rob;
-    a.ticks = c->d_sim_int;
-    a.status = c->d_sim_int + c->B;
-    a.goal = c->d_sim_goal;
-    a.n_obs = c->d_sim_nobs;
-    a.obs = c->d_sim_obs;
-    a.obs_old = c->d_sim_obs_old;
-    a.obs_speed = c->d_sim_speed;
-    a.det = c->d_sim_det;
-    a.hist = c->d_sim_hist;
-    a.meta = c->d_meta;
-    a.dt = f->dt;
-    a.r_robot = f->robot_radius;
-    a.r_obs = f->obstacle_radius;
-    a.goal_r = f->goal_radius;
-    a.turn_dist = f->turn_distance;
-    a.sigma_h = f->heading_sigma;
-    a.sigma_z = f->det_sigma;
-    a.cos_d = std::cos(f->turn_max);  // host libm (C25)
-    a.sin_d = std::sin(f->turn_max);
-    for (int k = 0; k < 37; ++k) a.cos_bins[k] = std::cos(k * 5.0 * M_PI / 180.0);
-    a.seed = f->seed;
-    a.max_ticks = f->max_ticks;
-    return a;
-}
-}  // namespace
-
-TWG_API twg_status twg_sim_reset(twg_ctx* c, int32_t b, const twg_robot* robot, int32_t goal_x, int32_t goal_y,
-                                 const double* obstacles, int32_t n, const twg_sim_cfg* cfg) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (!robot || b < 0 || b >= c->B || n < 0 || (n > 0 && !obstacles) || !sim_cfg_ok(cfg))
-        return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    if (c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "the simulator is not available on a row slab");
-    st = ensure_sim(c, std::max(n, 1));
-    if (st != TWG_OK) return st;
-    // Alg. 1 "Initialize the 2D map and harmonic potential values" (C36): static map + goal,
-    // no tracks, cold, relaxed to init_tol (checked every 100 sweeps)
-    EncodeReq r{b, *robot, goal_x, goal_y, 0, 0};
-    c->scen[b].encoded = false;
-    twg_warp_cfg wz;  // no tracks: the warp configuration is not used
-    std::memset(&wz, 0, sizeof(wz));
-    st = encode(c, {r}, nullptr, &wz, 0);
-    if (st < 0) return st;
-    std::vector<int> part(c->B, 0);
-    part[b] = 1;
-    twg_relax_cfg rc;
-    std::memset(&rc, 0, sizeof(rc));
-    rc.max_sweeps = cfg->init_max_sweeps;
-    rc.check_every = 100;
-    rc.tol = cfg->init_tol;
-    st = relax(c, &rc, part, nullptr, nullptr);
-    if (st != TWG_OK) return st;
-    // trial state
-    const int oc = c->sim_ocap;
-    char* h = nullptr;
-    const size_t bytes = 6 * sizeof(double) + 2 * sizeof(double) + (size_t)oc * 5 * sizeof(double);
-    TWG_CUDA(c, stage_alloc(c, bytes, reinterpret_cast<void**>(&h)));
-    double* hr = reinterpret_cast<double*>(h);
-    hr[0] = robot->x;
-    hr[1] = robot->y;
-    hr[2] = std::cos(robot->theta);  // host libm (C25)
-    hr[3] = std::sin(robot->theta);
-    hr[4] = robot->speed;
-    hr[5] = 0.0;
-    double* hg = hr + 6;
-    hg[0] = c->ox + ((double)goal_x + 0.5) * c->cs;
-    hg[1] = c->oy + ((double)goal_y + 0.5) * c->cs;
-    double* ho = hg + 2;
-    double* hs = ho + (size_t)oc * 4;
-    std::memset(ho, 0, (size_t)oc * 5 * sizeof(double));
-    for (int i = 0; i < n; ++i) {
-        for (int q = 0; q < 4; ++q) ho[4 * i + q] = obstacles[4 * i + q];
-        hs[i] = std::sqrt(obstacles[4 * i + 2] * obstacles[4 * i + 2] + obstacles[4 * i + 3] * obstacles[4 * i + 3]);
-    }
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_rob + 6 * b, hr, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_goal + 2 * b, hg, 2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_obs + (size_t)b * oc * 4, ho, (size_t)oc * 4 * sizeof(double),
-                                cudaMemcpyHostToDevice, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_speed + (size_t)b * oc, hs, (size_t)oc * sizeof(double),
-                                cudaMemcpyHostToDevice, c->stream));
-    TWG_CUDA(c, cudaMemsetAsync(c->d_sim_int + b, 0, sizeof(int), c->stream));          // ticks
-    TWG_CUDA(c, cudaMemsetAsync(c->d_sim_int + c->B + b, 0, sizeof(int), c->stream));   // running
-    TWG_CUDA(c, cudaMemsetAsync(c->d_sim_hist + 36 * b, 0, 36 * sizeof(int), c->stream));
-    int* hn = nullptr;
-    TWG_CUDA(c, stage_alloc(c, sizeof(int), reinterpret_cast<void**>(&hn)));
-    *hn = n;
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_sim_nobs + b, hn, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    SimArgs a = sim_args(c, cfg);
-    TWG_CUDA(c, launch_sim_sense(a, b, c->stream));
-    c->launches += 1;
-    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    for (int q = 0; q < 6; ++q) c->sim_rob[6 * b + q] = hr[q];
-    c->sim_ticks[b] = 0;
-    c->sim_status[b] = 0;
-    c->sim_nobs[b] = n;
-    c->scen[b].trk_n = 0;
-    return TWG_OK;
-}
-
-TWG_API twg_status twg_sim_tick(twg_ctx* c, const twg_sim_cfg* cfg, const twg_warp_cfg* warp,
-                                const twg_relax_cfg* rcfg, const twg_band_cfg* bcfg, const twg_tracker_cfg* tcfg,
-                                twg_sim_trial* out, int32_t* running) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (!sim_cfg_ok(cfg) || !warp || !rcfg || !bcfg || !tcfg) return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    if (!c->d_sim_rob) return fail(c, TWG_E_INVALID_ARG, "twg_sim_tick before twg_sim_reset");
-    std::vector<int> act;
-    for (int b = 0; b < c->B; ++b)
-        if (c->sim_status[b] == 0) act.push_back(b);
-    int worst = 0;
-    if (!act.empty()) {
-        // f1: tracker tick on this tick's detections
-        std::vector<TrkReq> rq(act.size());
-        for (size_t k = 0; k < act.size(); ++k) {
-            const int b = act[k];
-            rq[k].b = b;
-            rq[k].n = c->scen[b].trk_n;
-            rq[k].m = c->sim_nobs[b];
-            rq[k].det_off = (int64_t)b * c->sim_ocap;
-        }
-        std::vector<int> nout;
-        st = track_core(c, rq, c->d_sim_det, warp, tcfg, nout);
-        if (st < 0) return st;
-        worst = std::max(worst, (int)st);
-        // a1-a9 from the resident tracks
-        std::vector<EncodeReq> reqs;
-        for (int b : act) {
-            twg_robot rb;
-            rb.x = c->sim_rob[6 * b];
-            rb.y = c->sim_rob[6 * b + 1];
-            rb.theta = std::atan2(c->sim_rob[6 * b + 3], c->sim_rob[6 * b + 2]);  // host libm (C25)
-            rb.speed = c->sim_rob[6 * b + 4];
-            reqs.push_back(EncodeReq{b, rb, c->scen[b].gx, c->scen[b].gy, c->scen[b].trk_n, 0});
-        }
-        st = encode(c, reqs, nullptr, warp, rcfg->warm_start, true);
-        if (st < 0) return st;
-        std::vector<int> part(c->B, 0);
-        for (int b : act) part[b] = 1;
-        st = relax(c, rcfg, part, nullptr, nullptr);
-        if (st != TWG_OK) return st;
-        st = path(c, act, bcfg);
-        if (st != TWG_OK) return st;
-        // simulator step + next detections
-        SimArgs a = sim_args(c, cfg);
-        TWG_CUDA(c, launch_sim_move(a, c->stream));
-        TWG_CUDA(c, launch_sim_sense(a, -1, c->stream));
-        c->launches += 2;
-    }
-    // read back the trial states
-    const size_t B = c->B;
-    char* h = nullptr;
-    TWG_CUDA(c, stage_alloc(c, B * 6 * sizeof(double) + 2 * B * sizeof(int), reinterpret_cast<void**>(&h)));
-    double* hr = reinterpret_cast<double*>(h);
-    int* hi = reinterpret_cast<int*>(hr + 6 * B);
-    TWG_CUDA(c, cudaMemcpyAsync(hr, c->d_sim_rob, B * 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    TWG_CUDA(c, cudaMemcpyAsync(hi, c->d_sim_int, 2 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    int nrun = 0;
-    for (size_t b = 0; b < B; ++b) {
-        for (int q = 0; q < 6; ++q) c->sim_rob[6 * b + q] = hr[6 * b + q];
-        c->sim_ticks[b] = hi[b];
-        c->sim_status[b] = hi[B + b];
-        nrun += c->sim_status[b] == 0;
-        if (out) {
-            out[b].x = hr[6 * b];
-            out[b].y = hr[6 * b + 1];
-            out[b].hx = hr[6 * b + 2];
-            out[b].hy = hr[6 * b + 3];
-            out[b].speed = hr[6 * b + 4];
-            out[b].length = hr[6 * b + 5];
-            out[b].ticks = hi[b];
-            out[b].status = hi[B + b];
-        }
-    }
-    if (running) *running = nrun;
-    return (twg_status)worst;
-}
-
-TWG_API twg_status twg_sim_histogram(twg_ctx* c, int32_t b, int32_t* hist) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (!hist || b < 0 || b >= c->B || !c->d_sim_hist) return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    TWG_CUDA(c, cudaMemcpyAsync(hist, c->d_sim_hist + 36 * b, 36 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    return TWG_OK;
-}
-
-TWG_API twg_status twg_walk_from(twg_ctx* c, int32_t b, int32_t x, int32_t y, int32_t max_cells, int32_t* cells_xy,
-                                 int32_t* n_cells, int32_t* code, int32_t* next_xy) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (b < 0 || b >= c->B || x < 0 || x >= c->W || y < c->ghost || y >= c->H - c->ghost || max_cells < 0 || !code)
-        return fail(c, TWG_E_INVALID_ARG, "bad argument (the start must lie in the owned rows)");
-    int* d = nullptr;
-    TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&d), (4 + 2 * (size_t)std::max(max_cells, 1)) * sizeof(int),
-                                c->stream));
-    const float* f = c->u[c->cur[b]] + (int64_t)b * c->sstride;
-    TWG_CUDA(c, launch_walk_from(f, c->P, c->W, c->H, c->ghost, c->H - c->ghost, x, y, max_cells, d + 4, d, c->stream));
-    c->launches += 1;
-    int h[4];
-    TWG_CUDA(c, cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    if (cells_xy && h[1] > 0)
-        TWG_CUDA(c, cudaMemcpy(cells_xy, d + 4, (size_t)h[1] * 2 * sizeof(int), cudaMemcpyDeviceToHost));
-    TWG_CUDA(c, cudaFreeAsync(d, c->stream));
-    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    *code = h[0];
-    if (n_cells) *n_cells = h[1];
-    if (next_xy) {
-        next_xy[0] = h[2];
-        next_xy[1] = h[3];
-    }
-    return TWG_OK;
-}
-
-TWG_API twg_status twg_index_matrix(twg_ctx* c, int32_t b, uint8_t* out) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (!out || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    st = ensure_params(c, 1);
-    if (st != TWG_OK) return st;
-    ScenParams sp;
-    std::memset(&sp, 0, sizeof(sp));
-    sp.b = b;
-    sp.cur = c->cur[b];
-    void* hp = nullptr;
-    TWG_CUDA(c, stage_alloc(c, sizeof(ScenParams), &hp));
-    std::memcpy(hp, &sp, sizeof(sp));
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_params, hp, sizeof(ScenParams), cudaMemcpyHostToDevice, c->stream));
-    PathArgs p;
-    std::memset(&p, 0, sizeof(p));
-    p.u0 = c->u[0];
-    p.u1 = c->u[1];
-    p.P = c->P;
-    p.sstride = c->sstride;
-    p.W = c->W;
-    p.H = c->H;
-    p.params = c->d_params;
-    p.nscen = 1;
-    p.dir = c->d_dir;
-    p.istride = c->sstride;
-    TWG_CUDA(c, launch_index_dir(p, c->stream));
-    c->launches += 1;
-    // [H][P] -> [H][W] (cudaMemcpyDefault: out may be host or device)
-    TWG_CUDA(c, cudaMemcpy2DAsync(out, c->W, c->d_dir + (int64_t)b * c->sstride, c->P, c->W, c->H, cudaMemcpyDefault,
-                                  c->stream));
-    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    return TWG_OK;
-}
-
-TWG_API twg_status twg_warp_map(twg_ctx* c, const twg_robot* robot, double warp_spacing, int32_t* out) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (!out || !robot || !(warp_spacing > 0.0)) return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    const double cth = std::cos(robot->theta), sth = std::sin(robot->theta);  // host libm (C25)
-    const size_t bytes = (size_t)c->W * c->H * sizeof(int32_t);
-    int32_t* dst = out;
-    if (!is_device_ptr(out)) TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&dst), bytes, c->stream));
-    TWG_CUDA(c, launch_warp_map(dst, c->W, c->H, c->cs, c->ox, c->oy, robot->x, robot->y, cth, sth, warp_spacing,
-                                c->stream));
-    c->launches += 1;
-    if (dst != out) {
-        TWG_CUDA(c, cudaMemcpyAsync(out, dst, bytes, cudaMemcpyDeviceToHost, c->stream));
-        TWG_CUDA(c, cudaFreeAsync(dst, c->stream));
-    }
-    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    return TWG_OK;
-}
-
 TWG_API twg_status twg_field_ptr(twg_ctx* c, int32_t b, void** dev_ptr, int64_t* pitch) {
     if (!c || b < 0 || b >= c->B) return TWG_E_INVALID_ARG;
     if (dev_ptr) *dev_ptr = c->u[c->cur[b]] + (int64_t)b * c->sstride;
@@ -1596,3 +391,4 @@ TWG_API twg_status twg_profile_read(twg_ctx* c, double* relax_ms, int64_t* relax
 }
 
 TWG_API const char* twg_last_error(const twg_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+

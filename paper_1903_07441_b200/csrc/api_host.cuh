@@ -1,0 +1,60 @@
+// api_host.cuh -- host-side helpers shared by the C ABI translation units (host_core.cu, api*.cu).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "twg_kernels.cuh"
+
+namespace twg {
+namespace host {
+
+extern std::string g_create_err;  // message of the last failed twg_create
+
+twg_status fail(twg_ctx* c, twg_status st, const std::string& msg);
+
+#define TWG_CUDA(ctx, expr)                                                                                 \
+    do {                                                                                                    \
+        cudaError_t e_ = (expr);                                                                            \
+        if (e_ != cudaSuccess)                                                                              \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? TWG_E_NO_MEMORY : TWG_E_CUDA,                \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                                \
+    } while (0)
+
+template <class T>
+cudaError_t dev_alloc(T** p, size_t n) {
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T));
+}
+
+bool is_device_ptr(const void* p);
+bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P, int rows);
+bool make_idx_map(CUtensorMap* m, uint16_t* base, int H, int B, int64_t P);
+// Pinned staging ring for host->device copies (synchronises the stream when it wraps).
+cudaError_t stage_alloc(twg_ctx* c, size_t bytes, void** out);
+twg_status ensure_track_cap(twg_ctx* c, int cap);
+twg_status ensure_params(twg_ctx* c, int n);
+twg_status ensure_path_cap(twg_ctx* c, int max_len, int max_smooth);
+twg_status check_ctx(twg_ctx* c);
+
+struct EncodeReq {
+    int b;
+    twg_robot robot;
+    int gx, gy;
+    int n;
+    int64_t track_off;  // offset into the caller's track array
+};
+
+twg_status validate(twg_ctx* c, const EncodeReq& r, int* rcx, int* rcy);
+// Rows a1-a3 for a list of scenarios (resident: use the tracker tables already in d_tracks).
+twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_track* tracks, const twg_warp_cfg* wc,
+                  int warm_req, bool resident = false);
+// Rows a4-a6 for the scenarios with part[b] != 0.
+twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& part, int* sweeps_done,
+                 float* residual);
+// Rows a7-a9 for a list of scenarios (results stay on the device).
+twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg);
+// Row f1 tick for the requests rq (det_off relative to `det`, a device array of (x, y) pairs).
+twg_status track_core(twg_ctx* c, std::vector<TrkReq> rq, const double2* det, const twg_warp_cfg* wc,
+                      const twg_tracker_cfg* cfg, std::vector<int>& n_out);
+
+}  // namespace host
+}  // namespace twg
