@@ -242,6 +242,8 @@ __device__ void bitonic_sort(ulonglong2* v, int N) {
 
 constexpr int kSmemPairs = 4096;
 
+__device__ __forceinline__ int block_scan(int v, int* sw, int* total);
+
 __global__ void __launch_bounds__(1024) k_trk_assoc(TrackArgs t) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int k = blockIdx.x;
@@ -260,15 +262,50 @@ __global__ void __launch_bounds__(1024) k_trk_assoc(TrackArgs t) {
     for (int i = threadIdx.x; i < N; i += blockDim.x) v[i] = i < K ? list[i] : pad;
     __syncthreads();
     bitonic_sort(v, N);
-    // bitmaps of taken tracks and detections
+    // bitmaps of taken tracks and detections, and the number of gated pairs per track / detection
     unsigned* tbits = reinterpret_cast<unsigned*>(smem + kSmemPairs * sizeof(ulonglong2));
     unsigned* dbits = tbits + (t.cap + 31) / 32;
     const int nw = (t.cap + 31) / 32 + (t.mcap + 31) / 32;
+    int* cnt_t = reinterpret_cast<int*>(tbits + nw);
+    int* cnt_d = cnt_t + t.cap;
     for (int i = threadIdx.x; i < nw; i += blockDim.x) tbits[i] = 0u;
+    for (int i = threadIdx.x; i < t.cap + t.mcap; i += blockDim.x) cnt_t[i] = 0;
     __syncthreads();
+    for (int q = threadIdx.x; q < K; q += blockDim.x) {
+        atomicAdd(&cnt_t[(int)(v[q].y >> 32)], 1);
+        atomicAdd(&cnt_d[(int)(v[q].y & 0xffffffffu)], 1);
+    }
+    __syncthreads();
+    // A pair whose track and detection are in no other gated pair is taken whatever the order: accept
+    // those in parallel.  The greedy outcome of the others depends only on each other (any pair
+    // sharing an end with one of them is itself contested), so the sequential scan below runs over
+    // the contested pairs alone, in the same sorted order -- the same result as scanning all pairs.
+    const int64_t tb = (int64_t)rq.b * t.cap;
+    __shared__ int s_tot[32];
+    int nc = 0;
+    for (int q0 = 0; q0 < K; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        ulonglong2 pr = make_ulonglong2(0ull, 0ull);
+        int contested = 0;
+        if (q < K) {
+            pr = v[q];
+            const int i = (int)(pr.y >> 32), j = (int)(pr.y & 0xffffffffu);
+            if (cnt_t[i] == 1 && cnt_d[j] == 1) {
+                atomicOr(&tbits[i >> 5], 1u << (i & 31));
+                atomicOr(&dbits[j >> 5], 1u << (j & 31));
+                t.match[tb + i] = j;
+            } else {
+                contested = 1;
+            }
+        }
+        int tot;
+        const int pos = nc + block_scan(contested, s_tot, &tot);  // (block_scan synchronises)
+        if (contested) v[pos] = pr;  // stable, in place: pos <= q and this chunk was read above
+        nc += tot;
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
-        const int64_t tb = (int64_t)rq.b * t.cap;
-        for (int q = 0; q < K; ++q) {
+        for (int q = 0; q < nc; ++q) {
             const ulonglong2 p = v[q];
             const int i = (int)(p.y >> 32), j = (int)(p.y & 0xffffffffu);
             const unsigned ti = 1u << (i & 31), dj = 1u << (j & 31);
@@ -331,29 +368,27 @@ __device__ __forceinline__ int block_scan(int v, int* sw, int* total) {
     return excl;
 }
 
+// Positions of the surviving tracks and of the spawned ones (one CTA per request, integer block
+// scans only): pos_t[i] (in the match array, free after k_trk_update) and pos_d[j] (in the pair list,
+// free after k_trk_assoc), -1 when pruned, matched or beyond the capacity; then k_trk_scatter moves the
+// 160-byte tracks with the whole grid.
 __global__ void __launch_bounds__(1024) k_trk_compact(TrackArgs t) {
     __shared__ int sw[32];
     const int k = blockIdx.x;
     const TrkReq& rq = t.req[k];
     if (t.flags[k] & kTrkOverflow) return;
     const int64_t tb = (int64_t)rq.b * t.cap;
+    int* pos_d = reinterpret_cast<int*>(t.pairs + (int64_t)k * t.pcap);
     const int limit = rq.limit;
     int pos = 0;
     bool trunc = false;
     for (int i0 = 0; i0 < rq.n; i0 += blockDim.x) {
         const int i = i0 + threadIdx.x;
-        const int mis = i < rq.n ? t.mis_new[tb + i] : 0;
-        const int keep = (i < rq.n && mis <= t.prune_after) ? 1 : 0;
+        const int keep = (i < rq.n && t.mis_new[tb + i] <= t.prune_after) ? 1 : 0;
         int tot;
         const int p = pos + block_scan(keep, sw, &tot);
-        if (keep) {
-            if (p < limit) {
-                t.trk[tb + p] = t.pred[tb + i];
-                t.missed[tb + p] = mis;
-            } else {
-                trunc = true;
-            }
-        }
+        if (i < rq.n) t.match[tb + i] = keep && p < limit ? p : -1;
+        trunc |= keep && p >= limit;
         pos += tot;
     }
     for (int j0 = 0; j0 < rq.m; j0 += blockDim.x) {
@@ -361,38 +396,56 @@ __global__ void __launch_bounds__(1024) k_trk_compact(TrackArgs t) {
         const int sp = (j < rq.m && !t.used[(int64_t)k * t.mcap + j]) ? 1 : 0;
         int tot;
         const int p = pos + block_scan(sp, sw, &tot);
-        if (sp) {
-            if (p < limit) {
-                const double2 z = t.det[rq.det_off + j];
-                twg_track o;
-#pragma unroll
-                for (int q = 0; q < 16; ++q) o.P[q] = 0.0;
-                o.x[0] = z.x;
-                o.x[1] = z.y;
-                o.x[2] = 0.0;
-                o.x[3] = 0.0;
-                o.P[0] = t.var_pos;
-                o.P[5] = t.var_pos;
-                o.P[10] = t.var_vel;
-                o.P[15] = t.var_vel;
-                t.trk[tb + p] = o;
-                t.missed[tb + p] = 0;
-            } else {
-                trunc = true;
-            }
-        }
+        if (j < rq.m) pos_d[j] = sp && p < limit ? p : -1;
+        trunc |= sp && p >= limit;
         pos += tot;
     }
     if (__syncthreads_or(trunc) && threadIdx.x == 0) atomicOr(&t.flags[k], kTrkTruncated);
     if (threadIdx.x == 0) t.n_out[k] = min(pos, limit);
 }
 
+__global__ void k_trk_scatter(TrackArgs t) {
+    const int k = blockIdx.y;
+    const TrkReq& rq = t.req[k];
+    if (t.flags[k] & kTrkOverflow) return;
+    const int64_t tb = (int64_t)rq.b * t.cap;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < rq.n) {
+        const int p = t.match[tb + q];
+        if (p >= 0) {
+            t.trk[tb + p] = t.pred[tb + q];
+            t.missed[tb + p] = t.mis_new[tb + q];
+        }
+    }
+    if (q < rq.m) {
+        const int p = reinterpret_cast<const int*>(t.pairs + (int64_t)k * t.pcap)[q];
+        if (p >= 0) {
+            const double2 z = t.det[rq.det_off + q];
+            twg_track o;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o.P[e] = 0.0;
+            o.x[0] = z.x;
+            o.x[1] = z.y;
+            o.x[2] = 0.0;
+            o.x[3] = 0.0;
+            o.P[0] = t.var_pos;
+            o.P[5] = t.var_pos;
+            o.P[10] = t.var_vel;
+            o.P[15] = t.var_vel;
+            t.trk[tb + p] = o;
+            t.missed[tb + p] = 0;
+        }
+    }
+}
+
 cudaError_t launch_track_step(const TrackArgs& t, int nreq, int max_n, int max_m, int* n_launch, cudaStream_t st) {
     static unsigned long long init_mask = 0;
-    const size_t smem = kSmemPairs * sizeof(ulonglong2) + ((t.cap + 31) / 32 + (t.mcap + 31) / 32) * sizeof(unsigned);
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    const size_t smem = kSmemPairs * sizeof(ulonglong2) + ((t.cap + 31) / 32 + (t.mcap + 31) / 32) * sizeof(unsigned) +
+                        (size_t)(t.cap + t.mcap) * sizeof(int);
+    constexpr size_t kMaxDyn = 227 * 1024 - 1024;  // leaves room for the kernel's static shared memory
+    if (smem > kMaxDyn) return cudaErrorInvalidValue;
     if (first_on_device(init_mask))
-        cudaFuncSetAttribute(k_trk_assoc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_trk_assoc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDyn);
     const int nm = std::max(std::max(max_n, max_m), 1);
     k_trk_predict<<<dim3((nm + 127) / 128, nreq), 128, 0, st>>>(t);
     const int tiles = ((max_n + kPairTile - 1) / kPairTile) * ((max_m + kPairTile - 1) / kPairTile);
@@ -400,7 +453,8 @@ cudaError_t launch_track_step(const TrackArgs& t, int nreq, int max_n, int max_m
     k_trk_assoc<<<nreq, 1024, smem, st>>>(t);
     k_trk_update<<<dim3((std::max(max_n, 1) + 127) / 128, nreq), 128, 0, st>>>(t);
     k_trk_compact<<<nreq, 1024, 0, st>>>(t);
-    if (n_launch) *n_launch = 5;
+    k_trk_scatter<<<dim3((nm + 127) / 128, nreq), 128, 0, st>>>(t);
+    if (n_launch) *n_launch = 6;
     return cudaGetLastError();
 }
 
@@ -411,6 +465,7 @@ void preload_track_kernels() {
     cudaFuncGetAttributes(&a, k_trk_assoc);
     cudaFuncGetAttributes(&a, k_trk_update);
     cudaFuncGetAttributes(&a, k_trk_compact);
+    cudaFuncGetAttributes(&a, k_trk_scatter);
     cudaGetLastError();
 }
 
