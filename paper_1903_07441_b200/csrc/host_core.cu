@@ -260,10 +260,11 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     if (st != TWG_OK) return st;
     st = ensure_params(c, ns);
     if (st != TWG_OK) return st;
-    // tracks -> [B][cap]: one contiguous copy (device input: in place; host input: through the pinned
-    // staging ring and one H2D copy) and one scatter kernel for every scenario of the call
+    // caller tracks: device input is read in place, host input goes through the pinned staging ring
+    // in one H2D copy; k_track_predict copies them into the [B][cap] resident table as it reads them
+    const twg_track* src = nullptr;
     if (total > 0 && !resident) {
-        const twg_track* src = tracks;
+        src = tracks;
         if (!is_device_ptr(tracks)) {
             if (c->track_tmp_cap < total) {
                 if (c->d_track_tmp) cudaFree(c->d_track_tmp);
@@ -279,26 +280,7 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
                                         c->stream));
             src = c->d_track_tmp - first;  // offsets below are relative to the caller's array
         }
-        std::vector<int> off(ns + 1), sb(ns);
-        for (int k = 0; k < ns; ++k) {
-            off[k] = (int)reqs[k].track_off;
-            sb[k] = reqs[k].b;
-        }
-        off[ns] = (int)(reqs[ns - 1].track_off + reqs[ns - 1].n);
-        if (c->track_off_cap < 2 * ns + 1) {
-            if (c->d_track_off) cudaFree(c->d_track_off);
-            c->d_track_off = nullptr;
-            TWG_CUDA(c, dev_alloc(&c->d_track_off, 2 * ns + 1));
-            c->track_off_cap = 2 * ns + 1;
-        }
-        int* hs = nullptr;
-        TWG_CUDA(c, stage_alloc(c, (2 * ns + 1) * sizeof(int), reinterpret_cast<void**>(&hs)));
-        std::memcpy(hs, off.data(), (ns + 1) * sizeof(int));
-        std::memcpy(hs + ns + 1, sb.data(), ns * sizeof(int));
-        TWG_CUDA(c, cudaMemcpyAsync(c->d_track_off, hs, (2 * ns + 1) * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        TWG_CUDA(c, launch_scatter_tracks(src, c->d_track_off, ns, c->d_track_off + ns + 1, c->d_tracks, c->d_missed,
-                                          c->track_cap, c->stream));
-        c->launches += 1;
+        for (int k = 0; k < ns; ++k) ps[k].track_off = reqs[k].track_off;
     }
     // per-scenario params + cfg (pinned staging, one copy each)
     WarpCfgDev w;
@@ -330,6 +312,8 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     e.nscen = ns;
     e.wcfg = c->d_wcfg;
     e.tracks = c->d_tracks;
+    e.src = src;
+    e.missed = c->d_missed;
     e.cap = c->track_cap;
     e.t_out = c->d_t;
     e.j_out = c->d_j;

@@ -76,7 +76,14 @@ __global__ void k_track_predict(EncodeArgs e) {
     if (i >= sp.n_tracks) return;
     const int b = sp.b;
     const int64_t slot = (int64_t)b * e.cap + i;
-    const twg_track tr = e.tracks[slot];
+    twg_track tr;
+    if (e.src) {  // caller-supplied tracks replace the resident table (f1); copied here, no scatter pass
+        tr = e.src[sp.track_off + i];
+        e.tracks[slot] = tr;
+        e.missed[slot] = 0;
+    } else {
+        tr = e.tracks[slot];
+    }
     const WarpCfgDev& w = *e.wcfg;
     // a1: warp radius (Eq. 15 with the P:463-465 centre, closed form C16) from x_hat (C24)
     const double dx = tr.x[0] - sp.xr;
@@ -204,18 +211,6 @@ __global__ void k_set_goal(EncodeArgs e) {
     (sp.cur ? e.u1 : e.u0)[(int64_t)sp.b * e.sstride + (int64_t)sp.gy * e.P + sp.gx] = 1.0f;
 }
 
-__global__ void k_scatter_tracks(const twg_track* __restrict__ src, const int* __restrict__ off, int nscen,
-                                 const int* __restrict__ scen_b, twg_track* __restrict__ dst, int* __restrict__ missed,
-                                 int cap) {
-    pdl_enter();
-    const int k = blockIdx.y;
-    if (k >= nscen) return;
-    const int n = off[k + 1] - off[k];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        dst[(int64_t)scen_b[k] * cap + i] = src[off[k] + i];
-        missed[(int64_t)scen_b[k] * cap + i] = 0;  // caller-supplied tracks replace the tracker table (f1)
-    }
-}
 
 // Fresh context: every cell free at 0.5, pad columns fixed obstacles.
 __global__ void k_init_field(float* __restrict__ u, int64_t P, int64_t sstride, int W, int H) {
@@ -264,13 +259,6 @@ cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P,
     return cudaGetLastError();
 }
 
-cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nscen, const int* scen_b, twg_track* dst,
-                                  int* missed, int cap, cudaStream_t st) {
-    cudaError_t err = launch_pdl(k_scatter_tracks, dim3(1, nscen), dim3(128), 0, st, src, off, nscen, scen_b, dst,
-                                 missed, cap);
-    if (err != cudaSuccess) return err;
-    return cudaGetLastError();
-}
 
 __global__ void k_warp_map(int32_t* __restrict__ out, int W, int H, double cs, double ox, double oy, double xr,
                            double yr, double c, double s, double w);
@@ -284,7 +272,6 @@ void preload_stamp_kernels() {
     cudaFuncGetAttributes(&a, k_track_predict);
     cudaFuncGetAttributes(&a, k_stamp);
     cudaFuncGetAttributes(&a, k_set_goal);
-    cudaFuncGetAttributes(&a, k_scatter_tracks);
     cudaFuncGetAttributes(&a, k_convert);
     cudaFuncGetAttributes(&a, k_import);
     cudaGetLastError();

@@ -55,6 +55,7 @@ struct ScenParams {
     int cur;                     // buffer index holding the scenario's field
     int n_tracks;
     int n_prev_boxes;
+    int64_t track_off;           // first track of this scenario in EncodeArgs::src
 };
 
 struct WarpCfgDev {

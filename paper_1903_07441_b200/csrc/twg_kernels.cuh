@@ -64,7 +64,9 @@ struct EncodeArgs {
     const ScenParams* params;  // [nscen]
     int nscen;
     const WarpCfgDev* wcfg;
-    const twg_track* tracks;   // [B][cap]
+    twg_track* tracks;         // [B][cap] (the resident track table)
+    const twg_track* src;      // caller's tracks (copied into `tracks` by k_track_predict), or nullptr
+    int* missed;               // [B][cap] tracker miss counters, reset for copied tracks
     int cap;
     int* t_out;            // [B][cap]
     int* j_out;
@@ -75,8 +77,7 @@ struct EncodeArgs {
 };
 cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_tracks, int any_cold, int* n_launch,
                           cudaStream_t st);
-cudaError_t launch_scatter_tracks(const twg_track* src, const int* off, int nscen, const int* scen_b, twg_track* dst,
-                                  int* missed, int cap, cudaStream_t st);
+
 
 // k_track.cu (row f1: tracker tick)
 enum : int { kTrkTruncated = 1, kTrkSingular = 2, kTrkOverflow = 4 };
