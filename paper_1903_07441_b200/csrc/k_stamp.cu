@@ -287,7 +287,7 @@ cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_track
         ++nl;
     }
     if (max_prev_boxes > 0) {
-        if (cudaError_t err = launch_pdl(k_unstamp, dim3(max_prev_boxes, e.nscen), dim3(256), 0, st, e)) return err;
+        if (cudaError_t err = launch_pdl(k_unstamp, dim3(max_prev_boxes, e.nscen), dim3(1024), 0, st, e)) return err;
         ++nl;
     }
     const int sb = (e.nscen + 127) / 128;
@@ -296,7 +296,7 @@ cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_track
     if (max_tracks > 0) {
         if (cudaError_t err = launch_pdl(k_track_predict, dim3((max_tracks + 63) / 64, e.nscen), dim3(64), 0, st, e))
             return err;
-        if (cudaError_t err = launch_pdl(k_stamp, dim3(max_tracks, e.nscen), dim3(256), 0, st, e)) return err;
+        if (cudaError_t err = launch_pdl(k_stamp, dim3(max_tracks, e.nscen), dim3(512), 0, st, e)) return err;
         nl += 2;
     }
     if (cudaError_t err = launch_pdl(k_set_goal, dim3(sb), dim3(128), 0, st, e)) return err;
