@@ -388,3 +388,22 @@ def test_c5_full_batch_sampled_scenarios():
         if ref["walk_status"] == 0:
             assert np.array_equal(cells[b, : res[b].n_cells], ref["cells"])
             assert np.abs(sm[b, : res[b].n_smooth] - ref["smooth"]).max() <= 1e-4
+
+
+@pytest.mark.parametrize("T_", [3, 6])
+def test_batch_tolerance_stop_scenarios_finish_at_different_sweeps(T_):
+    # red-black batch with a tolerance: each scenario stops at its own check sweep; the fields of
+    # those that stopped early are moved back into place (k_fixup) -- all equal to the oracle
+    scs = [scene_random(f"bt{k}", 96, 2 + k, 2 * k, 60 + k) for k in range(4)]
+    pl = Planner(96, 96, 4, 0.1, (0.0, 0.0), device=0, stream=_stream())
+    for k, sc in enumerate(scs):
+        pl.set_static(sc.static, b=k)
+        pl.set_obstacles(k, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
+    sw, res = pl.relax(relax_cfg(max_sweeps=20000, check_every=7, tol=1e-5, temporal_depth=T_, sync_every=2))
+    got = set()
+    for k, sc in enumerate(scs):
+        ref = oracle.plan_step(sc, max_sweeps=20000, check_every=7, tol=1e-5, iters=0)
+        assert int(sw[k]) == ref["sweeps"] and np.float32(res[k]) == np.float32(ref["residual"])
+        _assert_field(pl.get_field(k, 1), ref["u"])
+        got.add(int(sw[k]))
+    assert len(got) > 1  # they really stopped at different sweeps
