@@ -373,7 +373,6 @@ int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows, int n_sm) {
     return std::max(best_h, 2);
 }
 
-// Rows a4-a6 for the scenarios whose participation flag is set.
 // Task lists and counters of the lexicographic mode: 32 x 32 tiles, tasks (sweep s, tile (i, j)) of
 // one launch of `sweeps` sweeps ordered by wavefront time i + j + 2 s, then s, then j.  Every
 // dependency of a task has a smaller time, so the order is topological.  Lists are cached per

@@ -17,6 +17,10 @@
 // sequence (C2; the library is compiled with -fmad=false, no fast-math, no
 // FTZ); colours are global (x + row_offset + y) parity; the residual is the
 // exact max of fabsf(new - old) over the free cells of the last sweep.
+//
+// Also here: k_jacobi (Eq. 1, relax mode 1), k_lex (lexicographic Eq. 2, mode 2, a persistent
+// tile wavefront), the bring-up kernel k_rb_simple, and the convergence control k_check /
+// k_fixup.  The launches of a relaxation chain use programmatic dependent launch.
 #include <algorithm>
 
 #include "twg_kernels.cuh"
