@@ -417,6 +417,8 @@ twg_status ensure_lex(twg_ctx* c) {
     return TWG_OK;
 }
 
+// Rows a4-a6 for the scenarios whose participation flag is set: launches of T sweeps (red-black),
+// single sweeps (Jacobi) or persistent launches (lexicographic), then k_check per check interval.
 twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& part, int* sweeps_done,
                  float* residual) {
     if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null relax cfg");
