@@ -407,3 +407,34 @@ def test_batch_tolerance_stop_scenarios_finish_at_different_sweeps(T_):
         _assert_field(pl.get_field(k, 1), ref["u"])
         got.add(int(sw[k]))
     assert len(got) > 1  # they really stopped at different sweeps
+
+
+@pytest.mark.slow
+def test_plan_loop_warm_parity_c2_long():
+    # SURVEY C2-style long warm plan loop (tick 0 cold to the exact fp32 fixed point, then S = 100
+    # per tick): every tick's field, cells and smoothed path bit-identical to the oracle replaying
+    # the same poses (192^2 so that the oracle's cold solve stays a few seconds)
+    sc0 = scene_random("long", 192, 4, 8, 3)
+    pl = _planner(sc0)
+    wc, bc = warp_cfg(), band_cfg(50, 4000, 8000)
+    prev = None
+    walks = 0
+    for tick in range(40):
+        sc = advance_scene(sc0, tick)
+        if tick == 0:
+            rc = relax_cfg(max_sweeps=400_000, check_every=500, tol=1e-38, warm_start=1)
+        else:
+            rc = relax_cfg(max_sweeps=100, warm_start=1)
+        st, res, cells, sm = pl.plan_step(0, [sc.robot], [sc.goal], sc.tracks, [sc.n_tracks], wc, rc, bc)
+        ref = oracle.plan_step(sc, max_sweeps=rc.max_sweeps, check_every=rc.check_every or None, tol=rc.tol,
+                               iters=50, max_len=4000, prev=prev)
+        prev = ref
+        r = res[0]
+        assert r.sweeps == ref["sweeps"], tick
+        assert np.array_equal(pl.get_field(0, 1), ref["u"]), tick
+        assert r.walk_status == ref["walk_status"], tick
+        if r.walk_status == T.OK:
+            walks += 1
+            assert np.array_equal(cells[0, : r.n_cells], ref["cells"]), tick
+            assert np.array_equal(sm[0, : r.n_smooth], ref["smooth"]), tick
+    assert walks >= 30
