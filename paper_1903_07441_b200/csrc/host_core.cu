@@ -437,19 +437,33 @@ twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& p
     const float tol = cfg->tol;
     int check = (tol > 0.0f && cfg->check_every > 0) ? cfg->check_every : std::max(maxs, 1);
     const int sync_every = cfg->sync_every > 0 ? cfg->sync_every : 64;
-    // control arrays [done | cur | sweeps | where | res bits | res]: one copy (done = !participating,
-    // where = -1: not (yet) finished)
-    int* hs = nullptr;
-    TWG_CUDA(c, stage_alloc(c, 6 * B * sizeof(int), reinterpret_cast<void**>(&hs)));
-    for (int b = 0; b < B; ++b) {
-        hs[b] = part[b] ? 0 : 1;
-        hs[B + b] = c->cur[b];
-        hs[2 * B + b] = 0;
-        hs[3 * B + b] = -1;
-        hs[4 * B + b] = 0;
-        hs[5 * B + b] = 0;  // +0.0f
+    // control arrays [done | cur | sweeps | where | res bits | res]: when the buffer indices or the
+    // participation changed since the last call, one copy of the whole block; otherwise a kernel
+    // resets done / sweeps / where / residual, so consecutive relaxations stay a chain of kernels
+    // (PDL included) -- the row-slab intervals
+    bool all = true;
+    for (int b = 0; b < B; ++b) all = all && part[b];
+    bool same = (int)c->cur_cache.size() == B && (int)c->part_cache.size() == B;
+    for (int b = 0; same && b < B; ++b) same = c->cur_cache[b] == c->cur[b] && c->part_cache[b] == (part[b] ? 1 : 0);
+    if (!same || !all) {
+        int* hs = nullptr;
+        TWG_CUDA(c, stage_alloc(c, 6 * B * sizeof(int), reinterpret_cast<void**>(&hs)));
+        c->cur_cache.assign(B, 0);
+        c->part_cache.assign(B, 0);
+        for (int b = 0; b < B; ++b) {
+            hs[b] = part[b] ? 0 : 1;
+            hs[B + b] = c->cur_cache[b] = c->cur[b];
+            c->part_cache[b] = part[b] ? 1 : 0;
+            hs[2 * B + b] = 0;
+            hs[3 * B + b] = -1;
+            hs[4 * B + b] = 0;
+            hs[5 * B + b] = 0;  // +0.0f
+        }
+        TWG_CUDA(c, cudaMemcpyAsync(c->d_ctl, hs, 6 * B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    } else {
+        TWG_CUDA(c, launch_relax_init(c->d_done, c->d_sweeps, c->d_where, c->d_res_bits, c->d_res, B, c->stream));
+        c->launches += 1;
     }
-    TWG_CUDA(c, cudaMemcpyAsync(c->d_ctl, hs, 6 * B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     if (lex)
         TWG_CUDA(c, cudaMemsetAsync(c->d_lex_tdone, 0, (size_t)B * c->lex_tx * c->lex_ty * sizeof(int), c->stream));
     int nscen = 0;

@@ -402,6 +402,27 @@ cudaError_t launch_lex(const LexArgs& a, int n_sm, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------- convergence control (a6)
+// Reset the per-call control of a relaxation in which every scenario takes part and the buffer
+// indices are already on the device: done 0, sweeps 0, where -1, residual 0.
+__global__ void k_relax_init(int B, int* __restrict__ done, int* __restrict__ sweeps, int* __restrict__ where,
+                             unsigned* __restrict__ res_bits, float* __restrict__ res) {
+    pdl_wait();
+    pdl_trigger();
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    done[b] = 0;
+    sweeps[b] = 0;
+    where[b] = -1;
+    res_bits[b] = 0u;
+    res[b] = 0.0f;
+}
+
+cudaError_t launch_relax_init(int* done, int* sweeps, int* where, unsigned* res_bits, float* res, int B, cudaStream_t st) {
+    cudaError_t e = launch_pdl(k_relax_init, dim3((B + 127) / 128), dim3(128), 0, st, B, done, sweeps, where, res_bits, res);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 // After a chunk of `chunk` sweeps whose last launch accumulated the residual:
 // sweeps += chunk; stop when (sweeps % check_every == 0 && res < tol) or
 // sweeps == max_sweeps (C6).  `where` records which ping-pong buffer
@@ -492,6 +513,7 @@ void preload_relax_kernels() {
     cudaFuncGetAttributes(&a, k_lex);
     cudaFuncGetAttributes(&a, k_jacobi);
     cudaFuncGetAttributes(&a, k_check);
+    cudaFuncGetAttributes(&a, k_relax_init);
     cudaFuncGetAttributes(&a, k_fixup);
     cudaGetLastError();
 }

@@ -243,6 +243,7 @@ struct twg_ctx {
     twg::PathMeta* d_meta = nullptr;   // [B]
     uint16_t* d_idx = nullptr;         // index matrix (4-step descriptors) [B][H][P]
     uint8_t* d_dir = nullptr;          // index matrix (direction bytes) [B][H][P]
+    std::vector<int> cur_cache, part_cache;  // cur / participation as last uploaded (twg_relax)
     CUtensorMap idx_map;               // TMA view of d_idx for the walker's windows
     // pinned host staging
     void* h_stage = nullptr;

@@ -46,6 +46,7 @@ cudaError_t launch_warp_map(int32_t* out, int W, int H, double cs, double ox, do
                             double s, double w, cudaStream_t st);
 cudaError_t launch_rb_simple(float* u, int64_t P, int64_t sstride, int W, int H, int B, int color, int row_off,
                              const int* done, unsigned* res, cudaStream_t st);
+cudaError_t launch_relax_init(int* done, int* sweeps, int* where, unsigned* res_bits, float* res, int B, cudaStream_t st);
 cudaError_t launch_check(int B, int* done, int* sweeps, unsigned* res_bits, float* res_final, int* where, int chunk,
                          int check_every, int max_sweeps, float tol, const int* cur, int lp, cudaStream_t st);
 cudaError_t launch_init_field(float* u, int64_t P, int64_t sstride, int W, int H, int B, cudaStream_t st);

@@ -134,7 +134,7 @@ class SlabRelaxer:
     def relax(self, max_sweeps: int, check_every: int = 0, tol: float = 0.0):
         res, s = 0.0, 0
         for n, is_check, s in interval_schedule(max_sweeps, self.lay.k, check_every, tol):
-            r = self.backend.relax(n)
+            r = self.backend.relax(n, need_residual=is_check)
             if is_check:
                 res = self.ex.allreduce_max(r, self.device)
             if s < max_sweeps:
@@ -159,10 +159,11 @@ class TwgSlabBackend:
         self.pl = planner
         self.device = device
 
-    def relax(self, n: int) -> float:
+    def relax(self, n: int, need_residual: bool = True) -> float:
+        """n sweeps; the residual is read back (a host synchronisation) only when asked for."""
         from .twg import relax_cfg
-        _, res = self.pl.relax(relax_cfg(max_sweeps=n))
-        return float(res[0])
+        _, res = self.pl.relax(relax_cfg(max_sweeps=n), want_result=need_residual)
+        return float(res[0]) if need_residual else 0.0
 
     def walk_segment(self, x: int, yl: int, max_cells: int):
         """Walk from local cell (x, yl) until the goal, a hand-over or a dead end (twg_walk_from)."""
@@ -209,7 +210,7 @@ def relax_local_slabs(backends, layouts, max_sweeps: int, check_every: int = 0, 
     k = layouts[0].k
     res, s = 0.0, 0
     for n, is_check, s in interval_schedule(max_sweeps, k, check_every, tol):
-        rs = [b.relax(n) for b in backends]
+        rs = [b.relax(n, need_residual=is_check) for b in backends]
         if is_check:
             res = max(rs)
         if s < max_sweeps:

@@ -41,7 +41,7 @@ class OracleSlabBackend:
         self.u = np.ascontiguousarray(lay.local_slice(u_g, np.float32(0)))
         self.t = torch.from_numpy(self.u)
 
-    def relax(self, n):
+    def relax(self, n, need_residual=True):
         lay = self.lay
         _, r = self.o.relax_f32_ex(self.cls, self.u, n, n, 0.0, row_parity=lay.row_offset,
                                    res_rows=(lay.G, lay.local_h - lay.G))
