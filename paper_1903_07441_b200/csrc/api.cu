@@ -105,7 +105,8 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
                     c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
                     c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det,
                     c->d_sim_rob, c->d_sim_int, c->d_sim_goal, c->d_sim_nobs, c->d_sim_obs, c->d_sim_obs_old,
-                    c->d_sim_speed, c->d_sim_det, c->d_sim_hist, c->d_lex_tdone, c->d_lex_task};
+                    c->d_sim_speed, c->d_sim_det, c->d_sim_hist, c->d_lex_tdone, c->d_lex_task, c->d_spec,
+                    c->d_seg, c->d_seg_cells};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : c->lex_lists) cudaFree(e.second);

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -178,6 +179,15 @@ twg_status ensure_path_cap(twg_ctx* c, int max_len, int max_smooth) {
         TWG_CUDA(c, dev_alloc(&c->d_cells, B * nc));
         TWG_CUDA(c, dev_alloc(&c->d_wp, B * nc));
         c->path_len_cap = nc;
+        // the cells buffer no longer holds the previous walks: no markers from it (k_spec_mark)
+        TWG_CUDA(c, cudaMemsetAsync(c->d_meta, 0xff, B * sizeof(PathMeta), c->stream));
+        if (B <= (size_t)kSpecMaxB) {
+            if (c->d_seg_cells) cudaFree(c->d_seg_cells);
+            c->d_seg_cells = nullptr;
+            TWG_CUDA(c, dev_alloc(&c->d_seg_cells, B * kSpecMax * (size_t)(nc + 1)));
+            if (!c->d_spec) TWG_CUDA(c, dev_alloc(&c->d_spec, B));
+            if (!c->d_seg) TWG_CUDA(c, dev_alloc(&c->d_seg, B * (kSpecMax + 1)));
+        }
     }
     if (max_smooth > c->smooth_cap) {
         int nc = std::max(max_smooth, 256);
@@ -646,6 +656,13 @@ twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg)
     p.win_pitch = 256;  // k_walk window pitch (TMA zero-fills columns beyond the grid)
     p.istride = c->sstride;
     p.idx_map = c->idx_map;
+    // speculative segment walkers from markers on the previous path (k_spec_mark); TWG_NO_SPEC=1
+    // runs the single walker only (same results)
+    static const bool no_spec = [] { const char* e = std::getenv("TWG_NO_SPEC"); return e && e[0] == '1'; }();
+    p.spec = c->d_spec;
+    p.seg = c->d_seg;
+    p.seg_cells = c->d_seg_cells;
+    p.spec_on = (!no_spec && c->d_seg_cells) ? 1 : 0;
     int nl = 0;
     TWG_CUDA(c, launch_path(p, &nl, c->stream));
     c->launches += nl;

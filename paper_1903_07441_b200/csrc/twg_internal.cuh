@@ -72,6 +72,27 @@ struct TrkReq {  // one scenario of a tracker tick (row f1)
     int64_t det_off;  // first detection in TrackArgs::det
 };
 
+// Speculative segment walkers (k_walk, row a7): sample cells of the previous path become markers
+// in the direction bytes, and one walker per marker runs concurrently with the walker from the robot.
+constexpr int kSpecMax = 64;     // segment walkers per scenario
+constexpr int kSpecMinSeg = 32;  // minimum previous-path cells between two markers
+constexpr int kSpecMaxB = 4;     // contexts with at most this many scenarios speculate
+constexpr int kDirMarker = 8;    // direction byte of marker k: kDirMarker + k
+
+struct SpecTab {  // per scenario, written by k_spec_mark
+    int K;                // markers placed (sample k at previous-path cell (k + 1) S)
+    int pad;
+    int2 pos[kSpecMax];   // marker cell, (-1, -1) when the sample was out of grid or a duplicate
+    int orig[kSpecMax];   // the direction byte the marker replaced (restored by k_spec_stitch)
+};
+
+struct SegOut {  // per walker (0: from the robot, 1 + k: from marker k)
+    int state;   // 1 goal, 2 no path (obstacle, no neighbour, > max_len), 3 reached a marker
+    int n;       // cells counted from the walker's start cell (inclusive) to its end cell (inclusive)
+    int next;    // state 3: the marker reached
+    int pad;
+};
+
 struct PathMeta {  // per scenario, written by k_walk / k_band
     int n_cells;
     int status;
@@ -241,6 +262,9 @@ struct twg_ctx {
     float2* d_wp = nullptr;            // [B][path_len_cap]
     float2* d_smooth = nullptr;        // [B][smooth_cap]
     twg::PathMeta* d_meta = nullptr;   // [B]
+    twg::SpecTab* d_spec = nullptr;    // [B] markers of the speculative walk (B <= kSpecMaxB)
+    twg::SegOut* d_seg = nullptr;      // [B][kSpecMax + 1] walker results
+    int2* d_seg_cells = nullptr;       // [B][kSpecMax][path_len_cap + 1] segment cells
     uint16_t* d_idx = nullptr;         // index matrix (4-step descriptors) [B][H][P]
     uint8_t* d_dir = nullptr;          // index matrix (direction bytes) [B][H][P]
     std::vector<int> cur_cache, part_cache;  // cur / participation as last uploaded (twg_relax)

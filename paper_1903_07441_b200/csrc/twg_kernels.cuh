@@ -121,6 +121,10 @@ struct PathArgs {
     int win_pitch;         // walker window row pitch (cells) = 256; descriptor offsets use it
     int64_t istride;       // entries per scenario (H * P)
     CUtensorMap idx_map;   // M_idx as a 2D {P, H * B} uint16 tensor, box {256, 176}
+    SpecTab* spec;         // [B] (spec_on)
+    SegOut* seg;           // [B][kSpecMax + 1] (spec_on)
+    int2* seg_cells;       // [B][kSpecMax][len_cap + 1] (spec_on)
+    int spec_on;           // speculative segment walkers (k_spec_mark / k_walk / k_spec_stitch)
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
 cudaError_t launch_index_dir(const PathArgs& p, cudaStream_t st);  // k_index_dir alone (twg_index_matrix)
