@@ -68,7 +68,6 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     c->d_res = reinterpret_cast<float*>(c->d_ctl + 5 * B);
     c->d_flags = c->d_ctl + 6 * B;
     CK(dev_alloc(&c->d_meta, B));
-    CK(dev_alloc(&c->d_idx, cells));
     CK(dev_alloc(&c->d_dir, cells));
     CK(cudaMemsetAsync(c->mask, 0, B * c->H * c->W, c->stream));
     CK(cudaMemsetAsync(c->d_meta, 0, B * sizeof(PathMeta), c->stream));
@@ -88,7 +87,7 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
         if (!make_tmap(&c->tmap[0][t], c->u[0], c->W, c->H, c->B, c->P, 2 * t + 2) ||
             !make_tmap(&c->tmap[1][t], c->u[1], c->W, c->H, c->B, c->P, 2 * t + 2))
             return bail(TWG_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point unavailable or bad layout)");
-    if (!make_idx_map(&c->idx_map, c->d_idx, c->H, c->B, c->P))
+    if (!make_dir_map(&c->dir_map, c->d_dir, c->H, c->B, c->P))
         return bail(TWG_E_CUDA, "cuTensorMapEncodeTiled failed for the index matrix");
     CK(cudaStreamSynchronize(c->stream));
 #undef CK
@@ -102,7 +101,7 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_ctl,   c->d_meta,   c->d_tracks,   c->d_t,
                     c->d_j,      c->d_pred,    c->d_boxes, c->d_param_block, c->d_track_off, c->d_cells, c->d_wp,
-                    c->d_smooth, c->d_idx, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
+                    c->d_smooth, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
                     c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det,
                     c->d_sim_rob, c->d_sim_int, c->d_sim_goal, c->d_sim_nobs, c->d_sim_obs, c->d_sim_obs_old,
                     c->d_sim_speed, c->d_sim_det, c->d_sim_hist, c->d_lex_tdone, c->d_lex_task, c->d_spec,

@@ -27,7 +27,7 @@ cudaError_t dev_alloc(T** p, size_t n) {
 
 bool is_device_ptr(const void* p);
 bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P, int rows);
-bool make_idx_map(CUtensorMap* m, uint16_t* base, int H, int B, int64_t P);
+bool make_dir_map(CUtensorMap* m, uint8_t* base, int H, int B, int64_t P);
 // Pinned staging ring for host->device copies (synchronises the stream when it wraps).
 cudaError_t stage_alloc(twg_ctx* c, size_t bytes, void** out);
 twg_status ensure_track_cap(twg_ctx* c, int cap);

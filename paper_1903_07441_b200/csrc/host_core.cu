@@ -64,14 +64,14 @@ bool make_tmap(CUtensorMap* m, float* base, int W, int H, int B, int64_t P, int 
 
 // The index matrix as a 2D {P, H * B} uint16 tensor with box {256, 176}: one box lands in shared
 // memory as 176 rows of 256 contiguous descriptors (k_walk windows, row pitch 256).
-bool make_idx_map(CUtensorMap* m, uint16_t* base, int H, int B, int64_t P) {
+bool make_dir_map(CUtensorMap* m, uint8_t* base, int H, int B, int64_t P) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)H * (cuuint64_t)B};
-    cuuint64_t strides[1] = {(cuuint64_t)P * 2};
+    cuuint64_t strides[1] = {(cuuint64_t)P};
     cuuint32_t box[2] = {256, 176};  // may exceed P: out-of-range columns are zero-filled
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -651,11 +651,9 @@ twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg)
     p.len_cap = c->path_len_cap;
     p.smooth_cap = c->smooth_cap;
     p.meta = c->d_meta;
-    p.idx = c->d_idx;
     p.dir = c->d_dir;
-    p.win_pitch = 256;  // k_walk window pitch (TMA zero-fills columns beyond the grid)
     p.istride = c->sstride;
-    p.idx_map = c->idx_map;
+    p.dir_map = c->dir_map;
     // speculative segment walkers from markers on the previous path (k_spec_mark); TWG_NO_SPEC=1
     // runs the single walker only (same results)
     static const bool no_spec = [] { const char* e = std::getenv("TWG_NO_SPEC"); return e && e[0] == '1'; }();

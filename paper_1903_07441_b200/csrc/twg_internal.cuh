@@ -265,10 +265,9 @@ struct twg_ctx {
     twg::SpecTab* d_spec = nullptr;    // [B] markers of the speculative walk (B <= kSpecMaxB)
     twg::SegOut* d_seg = nullptr;      // [B][kSpecMax + 1] walker results
     int2* d_seg_cells = nullptr;       // [B][kSpecMax][path_len_cap + 1] segment cells
-    uint16_t* d_idx = nullptr;         // index matrix (4-step descriptors) [B][H][P]
     uint8_t* d_dir = nullptr;          // index matrix (direction bytes) [B][H][P]
     std::vector<int> cur_cache, part_cache;  // cur / participation as last uploaded (twg_relax)
-    CUtensorMap idx_map;               // TMA view of d_idx for the walker's windows
+    CUtensorMap dir_map;               // TMA view of d_dir for the walker's windows
     // pinned host staging
     void* h_stage = nullptr;
     size_t h_stage_bytes = 0;

@@ -116,11 +116,9 @@ struct PathArgs {
     float2* smooth;        // [B][smooth_cap]
     int len_cap, smooth_cap;
     PathMeta* meta;        // [B]
-    uint16_t* idx;         // index matrix M_idx as 4-step descriptors, [B][H][P] (Eq. 3)
     uint8_t* dir;          // index matrix M_idx as one direction byte per cell, [B][H][P]
-    int win_pitch;         // walker window row pitch (cells) = 256; descriptor offsets use it
     int64_t istride;       // entries per scenario (H * P)
-    CUtensorMap idx_map;   // M_idx as a 2D {P, H * B} uint16 tensor, box {256, 176}
+    CUtensorMap dir_map;   // M_idx as a 2D {P, H * B} uint8 tensor, box {256, 176} (k_walk windows)
     SpecTab* spec;         // [B] (spec_on)
     SegOut* seg;           // [B][kSpecMax + 1] (spec_on)
     int2* seg_cells;       // [B][kSpecMax][len_cap + 1] (spec_on)

@@ -19,7 +19,7 @@ from paper_1903_07441_b200 import Planner, band_cfg, relax_cfg, warp_cfg  # noqa
 from paper_1903_07441_b200 import twg as T  # noqa: E402
 from scenes import advance_scene, scene_random  # noqa: E402
 
-PATH_LAUNCHES_SPEC = 7  # index_dir, spec_mark, index_desc, walk, spec_stitch, band, resample
+PATH_LAUNCHES_SPEC = 6  # index_dir, spec_mark, walk, spec_stitch, band, resample
 
 
 def _cls(raw):
