@@ -38,7 +38,8 @@
  *    free/fixed flag: a free cell holding u >= 0 is stored as -u (sign bit
  *    set); a fixed cell is stored non-negative: obstacle +0.0 (phi = 1),
  *    goal +1.0 (phi = 0).  Any other non-negative value is a fixed Dirichlet
- *    cell with that u (test data, pin P8).  Outside the grid u = +0.0
+ *    cell with that u (test data, pin P8).  Every |u| must lie in [0, 1]
+ *    (the range of u = 1 - phi; the index kernel orders |u| on its bits).  Outside the grid u = +0.0
  *    (obstacle, C4).
  */
 #ifndef TWG_H
