@@ -126,3 +126,60 @@ def test_spec_walk_unconverged_fields_with_cycles():
         pl.relax(relax_cfg(max_sweeps=200_000, check_every=5000, tol=1e-38, warm_start=1))
         st, _, _ = _check_walk(pl, sc, 4 * sc0.W)
         assert st == T.OK
+
+
+def test_spec_walk_batch_and_single_scenario_steps():
+    # a 3-scenario context: markers are per scenario; plan steps over all scenarios and over one
+    # scenario (twg_plan_step with b) alternate, every walk equal to the oracle's on that field
+    scs = [scene_random("specb%d" % k, 256, 5, 6, 20 + k) for k in range(3)]
+    pl = Planner(256, 256, 3, scs[0].cell_size, scs[0].origin, device=0,
+                 stream=torch.cuda.current_stream().cuda_stream)
+    for b, sc in enumerate(scs):
+        pl.set_static(sc.static, b=b)
+    wc, ml = warp_cfg(), 2048
+    bc = band_cfg(10, ml, 2 * ml)
+    for tick in range(6):
+        cur = [advance_scene(sc, tick) for sc in scs]
+        rc = relax_cfg(max_sweeps=300_000 if tick == 0 else 200, check_every=5000 if tick == 0 else 0,
+                       tol=1e-38 if tick == 0 else 0.0, warm_start=1)
+        if tick % 2 == 0:
+            st, res, cells, _ = pl.plan_step(-1, [s.robot for s in cur], [s.goal for s in cur],
+                                             np.concatenate([s.tracks for s in cur]), [s.n_tracks for s in cur],
+                                             wc, rc, bc)
+            bs = range(3)
+        else:
+            b = tick % 3
+            st, res, cells, _ = pl.plan_step(b, [cur[b].robot], [cur[b].goal], cur[b].tracks, [cur[b].n_tracks],
+                                             wc, rc, bc)
+            bs = [b]
+        for i, b in enumerate(bs):
+            raw = pl.get_field(b, 0)
+            rst, rcells = oracle.walk(_cls(raw), np.abs(raw), oracle.robot_cell(cur[b]), ml)
+            assert res[i].walk_status == rst, (tick, b)
+            if rst == T.OK:
+                assert np.array_equal(cells[i, : res[i].n_cells], rcells), (tick, b)
+
+
+@pytest.mark.slow
+def test_spec_walk_c3_bench_configuration():
+    # the bench's C3 loop: converged 4096^2 field, then warm plan steps with moving tracks; each
+    # step's speculative walk equals the oracle walk on the same field
+    from scenes import scene_c3
+    sc0 = scene_c3(0)
+    pl = Planner(sc0.W, sc0.H, 1, sc0.cell_size, sc0.origin, device=0, stream=torch.cuda.current_stream().cuda_stream)
+    pl.set_static(sc0.static)
+    ml = 4 * (sc0.W + sc0.H)
+    bc = band_cfg(0, ml, 2 * ml)
+    pl.plan_step(0, [sc0.robot], [sc0.goal], sc0.tracks, [sc0.n_tracks], warp_cfg(),
+                 relax_cfg(max_sweeps=4_000_000, check_every=20000, tol=1e-38, warm_start=0, sync_every=4), bc,
+                 want_paths=False)
+    for k in range(1, 4):
+        sc = advance_scene(sc0, k)
+        n0 = pl.kernel_launches()
+        st, res, cells, _ = pl.plan_step(0, [sc.robot], [sc.goal], sc.tracks, [sc.n_tracks], warp_cfg(),
+                                         relax_cfg(max_sweeps=100, warm_start=1), bc)
+        raw = pl.get_field(0, 0)
+        rst, rcells = oracle.walk(_cls(raw), np.abs(raw), oracle.robot_cell(sc), ml)
+        assert res[0].walk_status == rst == T.OK
+        assert np.array_equal(cells[0, : res[0].n_cells], rcells)
+        assert len(rcells) > 5000
