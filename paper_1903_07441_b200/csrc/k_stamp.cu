@@ -49,17 +49,27 @@ __global__ void k_unstamp(EncodeArgs e) {
     }
 }
 
-__global__ void k_goal_reset(EncodeArgs e) {
-    pdl_enter();
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= e.nscen) return;
-    const ScenParams& sp = e.params[k];
+__device__ __forceinline__ void goal_reset_one(const EncodeArgs& e, const ScenParams& sp) {
     e.flags[sp.b] = 0;  // warning flags of this call (set by k_stamp, which runs after)
     if (!sp.warm || sp.old_gx < 0 || sp.old_gy < 0 || sp.old_gy >= e.H) return;
     if (sp.old_gx == sp.gx && sp.old_gy == sp.gy) return;
     const int b = sp.b;
     if (e.mask[((int64_t)b * e.H + sp.old_gy) * e.W + sp.old_gx]) return;
     (sp.cur ? e.u1 : e.u0)[(int64_t)b * e.sstride + (int64_t)sp.old_gy * e.P + sp.old_gx] = -1.0f;  // free, u = 1
+}
+
+__device__ __forceinline__ void set_goal_one(const EncodeArgs& e, const ScenParams& sp) {
+    if (sp.gy < 0 || sp.gy >= e.H) return;  // the goal lies in another row slab
+    (sp.cur ? e.u1 : e.u0)[(int64_t)sp.b * e.sstride + (int64_t)sp.gy * e.P + sp.gx] = 1.0f;
+}
+
+// Standalone launches for encodes without tracks; with tracks, k_track_predict resets the goal and
+// k_stamp sets it (one thread of the scenario's first CTA each).
+__global__ void k_goal_reset(EncodeArgs e) {
+    pdl_enter();
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= e.nscen) return;
+    goal_reset_one(e, e.params[k]);
 }
 
 // Round half away from zero of a non-negative double (C25; equals llround for x >= 0).
@@ -72,6 +82,7 @@ __device__ __forceinline__ long long round_half_away(double x) {
 __global__ void k_track_predict(EncodeArgs e) {
     pdl_enter();
     const ScenParams& sp = e.params[blockIdx.y];
+    if (blockIdx.x == 0 && threadIdx.x == 0) goal_reset_one(e, sp);  // before k_stamp (next launch)
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sp.n_tracks) return;
     const int b = sp.b;
@@ -179,6 +190,7 @@ __global__ void k_track_predict(EncodeArgs e) {
 __global__ void k_stamp(EncodeArgs e) {
     pdl_enter();
     const ScenParams& sp = e.params[blockIdx.y];
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_goal_one(e, sp);  // k_stamp never writes the goal cell
     if ((int)blockIdx.x >= sp.n_tracks) return;
     const int b = sp.b;
     const int64_t slot = (int64_t)b * e.cap + blockIdx.x;
@@ -206,9 +218,7 @@ __global__ void k_set_goal(EncodeArgs e) {
     pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= e.nscen) return;
-    const ScenParams& sp = e.params[k];
-    if (sp.gy < 0 || sp.gy >= e.H) return;  // the goal lies in another row slab
-    (sp.cur ? e.u1 : e.u0)[(int64_t)sp.b * e.sstride + (int64_t)sp.gy * e.P + sp.gx] = 1.0f;
+    set_goal_one(e, e.params[k]);
 }
 
 
@@ -291,16 +301,16 @@ cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_track
         ++nl;
     }
     const int sb = (e.nscen + 127) / 128;
-    if (cudaError_t err = launch_pdl(k_goal_reset, dim3(sb), dim3(128), 0, st, e)) return err;
-    ++nl;
-    if (max_tracks > 0) {
+    if (max_tracks > 0) {  // the goal reset / set ride on the first CTA of each scenario
         if (cudaError_t err = launch_pdl(k_track_predict, dim3((max_tracks + 63) / 64, e.nscen), dim3(64), 0, st, e))
             return err;
         if (cudaError_t err = launch_pdl(k_stamp, dim3(max_tracks, e.nscen), dim3(512), 0, st, e)) return err;
         nl += 2;
+    } else {
+        if (cudaError_t err = launch_pdl(k_goal_reset, dim3(sb), dim3(128), 0, st, e)) return err;
+        if (cudaError_t err = launch_pdl(k_set_goal, dim3(sb), dim3(128), 0, st, e)) return err;
+        nl += 2;
     }
-    if (cudaError_t err = launch_pdl(k_set_goal, dim3(sb), dim3(128), 0, st, e)) return err;
-    ++nl;
     if (n_launch) *n_launch = nl;
     return cudaGetLastError();
 }
