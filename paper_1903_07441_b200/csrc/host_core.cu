@@ -179,13 +179,14 @@ twg_status ensure_path_cap(twg_ctx* c, int max_len, int max_smooth) {
         TWG_CUDA(c, dev_alloc(&c->d_cells, B * nc));
         TWG_CUDA(c, dev_alloc(&c->d_wp, B * nc));
         c->path_len_cap = nc;
-        // the cells buffer no longer holds the previous walks: no markers from it (k_spec_mark)
-        TWG_CUDA(c, cudaMemsetAsync(c->d_meta, 0xff, B * sizeof(PathMeta), c->stream));
         if (B <= (size_t)kSpecMaxB) {
             if (c->d_seg_cells) cudaFree(c->d_seg_cells);
             c->d_seg_cells = nullptr;
             TWG_CUDA(c, dev_alloc(&c->d_seg_cells, B * kSpecMax * (size_t)(nc + 1)));
-            if (!c->d_spec) TWG_CUDA(c, dev_alloc(&c->d_spec, B));
+            if (!c->d_spec) {  // no markers before the first walk
+                TWG_CUDA(c, dev_alloc(&c->d_spec, B));
+                TWG_CUDA(c, cudaMemsetAsync(c->d_spec, 0, B * sizeof(SpecTab), c->stream));
+            }
             if (!c->d_seg) TWG_CUDA(c, dev_alloc(&c->d_seg, B * (kSpecMax + 1)));
         }
     }
@@ -654,7 +655,7 @@ twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg)
     p.dir = c->d_dir;
     p.istride = c->sstride;
     p.dir_map = c->dir_map;
-    // speculative segment walkers from markers on the previous path (k_spec_mark); TWG_NO_SPEC=1
+    // speculative segment walkers from markers on the previous path (k_index_dir); TWG_NO_SPEC=1
     // runs the single walker only (same results)
     static const bool no_spec = [] { const char* e = std::getenv("TWG_NO_SPEC"); return e && e[0] == '1'; }();
     p.spec = c->d_spec;

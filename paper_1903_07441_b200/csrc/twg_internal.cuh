@@ -79,11 +79,11 @@ constexpr int kSpecMinSeg = 32;  // minimum previous-path cells between two mark
 constexpr int kSpecMaxB = 4;     // contexts with at most this many scenarios speculate
 constexpr int kDirMarker = 8;    // direction byte of marker k: kDirMarker + k
 
-struct SpecTab {  // per scenario, written by k_spec_mark
-    int K;                // markers placed (sample k at previous-path cell (k + 1) S)
+struct SpecTab {  // per scenario: pos / K by k_spec_stitch (next walk's samples), orig by k_index_dir
+    int K;                // samples (sample k at cell (k + 1) S of the previous walk)
     int pad;
     int2 pos[kSpecMax];   // marker cell, (-1, -1) when the sample was out of grid or a duplicate
-    int orig[kSpecMax];   // the direction byte the marker replaced (restored by k_spec_stitch)
+    int orig[kSpecMax];   // the direction byte the marker replaced, -1 until placed (restored by k_spec_stitch)
 };
 
 struct SegOut {  // per walker (0: from the robot, 1 + k: from marker k)

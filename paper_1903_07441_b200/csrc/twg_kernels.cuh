@@ -122,7 +122,7 @@ struct PathArgs {
     SpecTab* spec;         // [B] (spec_on)
     SegOut* seg;           // [B][kSpecMax + 1] (spec_on)
     int2* seg_cells;       // [B][kSpecMax][len_cap + 1] (spec_on)
-    int spec_on;           // speculative segment walkers (k_spec_mark / k_walk / k_spec_stitch)
+    int spec_on;           // speculative segment walkers (markers in k_index_dir / k_walk / k_spec_stitch)
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
 cudaError_t launch_index_dir(const PathArgs& p, cudaStream_t st);  // k_index_dir alone (twg_index_matrix)
