@@ -1,4 +1,4 @@
-"""Speculative segment walkers (row a7, DESIGN.md "k_spec_mark / k_walk / k_spec_stitch"): the walk
+"""Speculative segment walkers (row a7, DESIGN.md "k_index_dir / k_walk / k_spec_stitch"): the walk
 assembled from the walker at the robot cell and the walkers at markers placed on the previous path
 must equal the single descent walk of the oracle (orc_walk, Alg. 1, C9) -- whatever the
 markers are: robot on a marker, markers on cells the new walk never visits, a moved goal, a walk
