@@ -162,6 +162,24 @@ def test_warp_map_bit_exact(W, H, theta, w):
         pl.warp_map(robot, 0.0)
 
 
+@pytest.mark.parametrize("w", [0.05, 0.35, 3.0])
+@pytest.mark.parametrize("centred", [False, True])
+def test_warp_map_bit_exact_large(w, centred):
+    # 2048^2 (4.2 M cells, hundreds of thousands on or next to ring boundaries at small w): the fp32
+    # screen of k_warp_map must hand every undecided cell to the fp64 sequence.  A robot at a cell
+    # centre gives a cell with d = 0 and rings through cell centres along the axes.
+    W = H = 2048
+    origin = (1000.3, -2000.7)
+    xr = origin[0] + (1000 + 0.5) * 0.1 if centred else origin[0] + 100.0123
+    yr = origin[1] + (700 + 0.5) * 0.1 if centred else origin[1] + 71.9
+    robot = (xr, yr, 0.0 if centred else 2.2, 0.4)
+    pl = Planner(W, H, 1, 0.1, origin, device=0, stream=_stream())
+    sc = Scene("wm", W, H, 0.1, origin, np.zeros((H, W), np.uint8), robot, (0, 0), np.zeros((0, 20)),
+               default_warp_cfg(), 0)
+    sc.warp.warp_spacing = w
+    assert np.array_equal(pl.warp_map(robot, w), oracle.warp_map(sc))
+
+
 def test_warp_map_agrees_with_track_labels():
     # a track sitting exactly at a cell centre gets that cell's warp number (rows a1 vs f3)
     sc = scene_random("wl", 256, 6, 30, 5)
