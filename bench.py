@@ -63,6 +63,7 @@ def _args():
     ap.add_argument("--batch", type=int, default=1024, help="c5: total scenarios")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--probe", action="store_true", help="launcher check: every rank prints its rank and exits")
     return ap.parse_args()
 
 
@@ -486,8 +487,31 @@ def run_c5(args):
         torch.distributed.destroy_process_group()
 
 
+def _launch_ranks(args) -> int:
+    """--gpus N > 1 without a torchrun environment: start N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 with this very command line; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = _args()
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        sys.exit(_launch_ranks(args))
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws_env} but --gpus {args.gpus}; refusing to run", file=sys.stderr)
+        sys.exit(2)
+    if args.probe:
+        ws, rank, local = _dist()
+        print(json.dumps({"probe": True, "rank": rank, "world_size": ws, "local_rank": local, "pid": os.getpid()}),
+              flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "c4":

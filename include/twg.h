@@ -237,8 +237,9 @@ TWG_API twg_status twg_set_static(twg_ctx* ctx, int32_t b, const uint8_t* occ);
  *      is the goal, the robot's cell stays free (C22).
  * warm = 0: every free cell restarts at 0.5 ("cleared");
  * warm = 1: every free cell keeps the value it holds, including cells fixed
- * in the previous call and free now (a released obstacle keeps u = 0, a
- * released goal u = 1) ("the values evolve slowly"; C7).
+ * in the previous call and free now (a released obstacle keeps u = 0), except
+ * a released goal, which restarts at u = 0 (a free cell at u = 1 would be a
+ * spurious maximum) ("the values evolve slowly"; C7).
  * tracks: n entries, host or device pointer (n may be 0); they also replace
  * the scenario's resident tracker table (missed counters 0).  tracks = NULL
  * with n = TWG_RESIDENT_TRACKS: use the resident table as left by

@@ -48,8 +48,6 @@ def lib():
         L = C.CDLL(_LIB)
         d, i32, i64, f32 = C.c_double, C.c_int32, C.c_int64, C.c_float
         P = C.c_void_p
-        L.orc_eq14_lhs.restype = d
-        L.orc_eq14_lhs.argtypes = [d] * 7
         L.orc_warp_radius.restype = d
         L.orc_warp_radius.argtypes = [d] * 6
         L.orc_warp_number.restype = i32
@@ -94,7 +92,7 @@ def lib():
         L.orc_warp_map.restype = None
         L.orc_warp_map.argtypes = [i32, i32, d, d, d, d, d, d, d, P]
         L.orc_init_u32.restype = None
-        L.orc_init_u32.argtypes = [i64, P, P, P]
+        L.orc_init_u32.argtypes = [i64, P, P, P, P]
         L.orc_init_u64.restype = None
         L.orc_init_u64.argtypes = [i64, P, P]
         L.orc_relax_f32.restype = i32
@@ -111,8 +109,6 @@ def lib():
         L.orc_bilerp.argtypes = [i32, i32, P, f32, f32]
         L.orc_band.restype = None
         L.orc_band.argtypes = [i32, i32, P, P, i32, P, i32, f32, f32]
-        L.orc_band_sequential.restype = None
-        L.orc_band_sequential.argtypes = [i32, i32, P, P, i32, P, i32, f32, f32]
         L.orc_resample.restype = i32
         L.orc_resample.argtypes = [i32, P, i32, P]
         L.orc_next_waypoint.restype = i32
@@ -126,10 +122,6 @@ def _p(a: np.ndarray):
 
 
 # ---------------------------------------------------------------- O1, O2
-def eq14_lhs(xr, yr, theta, xo, yo, rx):
-    return lib().orc_eq14_lhs(xr, yr, math.cos(theta), math.sin(theta), xo, yo, rx)
-
-
 def warp_radius(xr, yr, theta, xo, yo):
     return lib().orc_warp_radius(xr, yr, math.cos(theta), math.sin(theta), xo, yo)
 
@@ -196,15 +188,17 @@ def robot_cell(scene):
             int(math.floor((yr - scene.origin[1]) / scene.cell_size)))
 
 
-def init_u32(cls, u_prev=None):
-    """cold (u_prev None): goal 1, obstacle 0, free 0.5; warm: free cells keep u_prev (C7)."""
+def init_u32(cls, u_prev=None, cls_prev=None):
+    """cold (u_prev None): goal 1, obstacle 0, free 0.5; warm: free cells keep u_prev, a released
+    goal (cls_prev GOAL, free now) restarts at 0 (C7)."""
     cls = np.ascontiguousarray(cls, np.uint8)
     u = np.zeros(cls.shape, np.float32)
     if u_prev is None:
-        lib().orc_init_u32(cls.size, _p(cls), None, _p(u))
+        lib().orc_init_u32(cls.size, _p(cls), None, None, _p(u))
     else:
         up = np.ascontiguousarray(u_prev, np.float32)
-        lib().orc_init_u32(cls.size, _p(cls), _p(up), _p(u))
+        cp = None if cls_prev is None else np.ascontiguousarray(cls_prev, np.uint8)
+        lib().orc_init_u32(cls.size, _p(cls), _p(up), None if cp is None else _p(cp), _p(u))
     return u
 
 
@@ -354,13 +348,12 @@ def bilerp(u, px, py):
     return lib().orc_bilerp(W, H, _p(u), float(px), float(py))
 
 
-def band(cls, u, waypoints, iters=50, step=0.25, kt=1.0, sequential=False):
+def band(cls, u, waypoints, iters=50, step=0.25, kt=1.0):
     cls = np.ascontiguousarray(cls, np.uint8)
     u = np.ascontiguousarray(u, np.float32)
     H, W = u.shape
     w = np.ascontiguousarray(waypoints, np.float32).reshape(-1, 2).copy()
-    f = lib().orc_band_sequential if sequential else lib().orc_band
-    f(W, H, _p(cls), _p(u), w.shape[0], _p(w), int(iters), np.float32(step), np.float32(kt))
+    lib().orc_band(W, H, _p(cls), _p(u), w.shape[0], _p(w), int(iters), np.float32(step), np.float32(kt))
     return w
 
 
@@ -399,7 +392,7 @@ def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0
     if prev is None:
         u = init_u32(cls)
     else:
-        u = init_u32(cls, prev["u"])
+        u = init_u32(cls, prev["u"], prev.get("cls"))
     relax = relax_jacobi_f32 if jacobi else (relax_lex_f32 if lex else relax_f32)
     sweeps, res = relax(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol)
     if max_len is None:

@@ -38,20 +38,6 @@ enum { ORC_OK = 0, ORC_W_GOAL_SWALLOWED = 1, ORC_E_INVALID_ARG = -1, ORC_E_OUT_O
 /* O1  time-warp radius and warp number  (Eqs. 14-15; C16, C17)  */
 /* ------------------------------------------------------------------------ */
 
-/* Left-hand side of Eq. 14 for a given r_x, with the centre of
- * P:463-465 (x_c = x_r + 0.9 r_x cos(theta)) and r_y = r_x / 4.
- * Used by the pins to check the closed form below against the paper's
- * implicit definition. */
-double orc_eq14_lhs(double xr, double yr, double c, double s, double xo, double yo, double rx)
-{
-    double xc = xr + 0.9 * rx * c;
-    double yc = yr + 0.9 * rx * s;
-    double ry = rx / 4.0;
-    double A = c * (xo - xc) + s * (yo - yc);
-    double B = s * (xo - xc) - c * (yo - yc);
-    return (A * A) / (rx * rx) + (B * B) / (ry * ry);
-}
-
 /* Eq. 15 is implicit because (x_c, y_c) depend on r_x.
  * With a = c dx + s dy, b = s dx - c dy (dx = x_obj - x_r): the rotated
  * offsets from the centre are a - 0.9 r and b, so Eq. 15 squared reads
@@ -263,15 +249,19 @@ int32_t orc_classify(int32_t W, int32_t H, double cs, double ox, double oy,
 /* Field initialisation in u-space (C7).
  * cold (u_prev == NULL): goal 1, obstacle 0, free 0.5 ("initialized with 0.5").
  * warm: fixed-now cells take their fixed value; every free cell keeps the value
- * it held after the previous tick, including cells that were fixed then (an
- * obstacle cell released keeps u = 0, i.e. phi = 1) ("the values
- * evolve slowly anyways"). */
-void orc_init_u32(int64_t ncell, const uint8_t* cls, const float* u_prev, float* u)
+ * it held after the previous tick ("the values evolve slowly
+ * anyways"), so an obstacle cell released keeps u = 0 (phi = 1); the one
+ * exception is a released goal (cls_prev GOAL, free now), which restarts at
+ * u = 0 like a released obstacle instead of keeping u = 1: a free cell at the
+ * maximum value would be a spurious maximum of the field, the very trap of the
+ * descent walk that C7 avoids.  cls_prev may be NULL (no goal released). */
+void orc_init_u32(int64_t ncell, const uint8_t* cls, const float* u_prev, const uint8_t* cls_prev, float* u)
 {
     for (int64_t q = 0; q < ncell; ++q) {
         if (cls[q] == ORC_GOAL) u[q] = 1.0f;
         else if (cls[q] == ORC_OBSTACLE) u[q] = 0.0f;
         else if (u_prev == NULL) u[q] = 0.5f;
+        else if (cls_prev != NULL && cls_prev[q] == ORC_GOAL) u[q] = 0.0f;
         else u[q] = u_prev[q];
     }
 }
@@ -620,19 +610,6 @@ void orc_band(int32_t W, int32_t H, const uint8_t* cls, const float* u,
                 orc_band_point(W, H, cls, u, w + 2 * (i - 1), w + 2 * i, w + 2 * (i + 1), step, kt, o);
                 w[2 * i] = o[0]; w[2 * i + 1] = o[1];
             }
-}
-
-/* SPEC.md:235's literal sequential order (start to goal), oracle-only, used
- * by property tests of the band (not a parity target). */
-void orc_band_sequential(int32_t W, int32_t H, const uint8_t* cls, const float* u,
-                         int32_t n, float* w, int32_t iters, float step, float kt)
-{
-    for (int32_t it = 0; it < iters; ++it)
-        for (int32_t i = 1; i + 1 < n; ++i) {
-            float o[2];
-            orc_band_point(W, H, cls, u, w + 2 * (i - 1), w + 2 * i, w + 2 * (i + 1), step, kt, o);
-            w[2 * i] = o[0]; w[2 * i + 1] = o[1];
-        }
 }
 
 /* Resample (C15): each segment of length l is replaced by

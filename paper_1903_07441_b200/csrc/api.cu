@@ -246,11 +246,16 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
                                           cudaMemcpyDeviceToHost, c->stream));
     }
     TWG_CUDA(c, cudaStreamSynchronize(c->stream));
-    if (b >= 0 && (cells_xy || smooth_xy) && hm[b].status == TWG_OK) {
+    // copy the per-scenario results out of the staging ring now: the path read-back below takes a
+    // second staging region, which may wrap over (or reallocate) this one
+    const std::vector<PathMeta> vm(hm, hm + B);
+    const std::vector<int> vsw(hsw, hsw + B), vf(hf, hf + B);
+    const std::vector<float> vr(hr, hr + B);
+    if (b >= 0 && (cells_xy || smooth_xy) && vm[b].status == TWG_OK) {
         // one scenario: read back only the cells and points produced, through the pinned staging
         // buffer (the caller's arrays are usually pageable)
-        const int nc = std::min(hm[b].n_cells, bcfg->max_len);
-        const int nsm = std::min(hm[b].n_smooth, bcfg->max_smooth);
+        const int nc = std::min(vm[b].n_cells, bcfg->max_len);
+        const int nsm = std::min(vm[b].n_smooth, bcfg->max_smooth);
         const size_t bc = cells_xy ? (size_t)nc * sizeof(int2) : 0, bsm = smooth_xy ? (size_t)nsm * sizeof(float2) : 0;
         char* hp = nullptr;
         TWG_CUDA(c, stage_alloc(c, bc + bsm + 16, reinterpret_cast<void**>(&hp)));
@@ -267,16 +272,16 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
     for (int k = 0; k < ns; ++k) {
         const int q = bs[k];
         twg_plan_result& r = out[k];
-        r.sweeps = hsw[q];
-        r.residual = hr[q];
-        r.n_cells = hm[q].n_cells;
-        r.n_smooth = hm[q].status == TWG_OK ? hm[q].n_smooth : 0;
-        r.next_x = hm[q].next_x;
-        r.next_y = hm[q].next_y;
-        r.walk_status = hm[q].status;
+        r.sweeps = vsw[q];
+        r.residual = vr[q];
+        r.n_cells = vm[q].n_cells;
+        r.n_smooth = vm[q].status == TWG_OK ? vm[q].n_smooth : 0;
+        r.next_x = vm[q].next_x;
+        r.next_y = vm[q].next_y;
+        r.walk_status = vm[q].status;
         twg_status s = TWG_OK;
-        if (hm[q].status != TWG_OK) s = TWG_E_NO_PATH;
-        else if (hf[q]) s = TWG_W_GOAL_SWALLOWED;
+        if (vm[q].status != TWG_OK) s = TWG_E_NO_PATH;
+        else if (vf[q]) s = TWG_W_GOAL_SWALLOWED;
         else if (r.n_smooth > bcfg->max_smooth) s = TWG_W_TRUNCATED;
         r.status = s;
         if (s < 0 ? (worst >= 0 || s < worst) : (worst >= 0 && s > worst)) worst = s;

@@ -19,7 +19,7 @@
 // exact max of fabsf(new - old) over the free cells of the last sweep.
 //
 // Also here: k_jacobi (Eq. 1, relax mode 1), k_lex (lexicographic Eq. 2, mode 2, a persistent
-// tile wavefront), the bring-up kernel k_rb_simple, and the convergence control k_check /
+// tile wavefront), and the convergence control k_check /
 // k_fixup.  The launches of a relaxation chain use programmatic dependent launch.
 #include <algorithm>
 
@@ -181,36 +181,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     if (RESID) {
         const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(st.dmax));
         if (lane == 0 && m != 0u) atomicMax(&a.res[b], m);
-    }
-}
-
-// ---------------------------------------------------------------- bring-up kernel
-// One half-sweep (colour `color`) over the whole grid, in place (same-colour cells
-// never neighbour each other, so the pass is order-free).  Bit-identical to the
-// tile kernel and the oracle; used by the invariance tests.
-__global__ void k_rb_simple(float* __restrict__ u, int64_t P, int64_t sstride, int W, int H, int color, int row_off,
-                            const int* __restrict__ done, unsigned* __restrict__ res) {
-    const int b = blockIdx.z;
-    if (done != nullptr && done[b]) return;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    float* f = u + (int64_t)b * sstride;
-    float d = 0.0f;
-    if (x < W && y < H && ((x + y + row_off) & 1) == color) {
-        const float c = f[(int64_t)y * P + x];
-        if (is_free(c)) {
-            const float e = x + 1 < W ? fabsf(f[(int64_t)y * P + x + 1]) : 0.0f;
-            const float w = x > 0 ? fabsf(f[(int64_t)y * P + x - 1]) : 0.0f;
-            const float n = y > 0 ? fabsf(f[(int64_t)(y - 1) * P + x]) : 0.0f;
-            const float s = y + 1 < H ? fabsf(f[(int64_t)(y + 1) * P + x]) : 0.0f;
-            const float nv = 0.25f * ((e + w) + (n + s));
-            d = fabsf(-nv - c);
-            f[(int64_t)y * P + x] = -nv;
-        }
-    }
-    if (res != nullptr) {
-        const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(d));
-        if ((threadIdx.x & 31) == 0 && m != 0u) atomicMax(&res[b], m);
     }
 }
 
@@ -509,21 +479,12 @@ void preload_relax_kernels() {
     preload_T<1>(); preload_T<2>(); preload_T<3>(); preload_T<4>();
     preload_T<5>(); preload_T<6>(); preload_T<7>(); preload_T<8>();
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, k_rb_simple);
     cudaFuncGetAttributes(&a, k_lex);
     cudaFuncGetAttributes(&a, k_jacobi);
     cudaFuncGetAttributes(&a, k_check);
     cudaFuncGetAttributes(&a, k_relax_init);
     cudaFuncGetAttributes(&a, k_fixup);
     cudaGetLastError();
-}
-
-cudaError_t launch_rb_simple(float* u, int64_t P, int64_t sstride, int W, int H, int B, int color, int row_off,
-                             const int* done, unsigned* res, cudaStream_t st) {
-    dim3 blk(32, 8);
-    dim3 grid((W + 31) / 32, (H + 7) / 8, B);
-    k_rb_simple<<<grid, blk, 0, st>>>(u, P, sstride, W, H, color, row_off, done, res);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_check(int B, int* done, int* sweeps, unsigned* res_bits, float* res_final, int* where, int chunk,

@@ -4,7 +4,8 @@
 //   k_encode_cold     cold encode: free 0.5, static walls +0.0
 //   k_unstamp         warm encode: cells stamped last tick are released as free cells that keep
 //                     their value u = 0 (C7: warm start keeps every value)
-//   k_goal_reset      warm encode: the previous goal cell is released as a free cell keeping u = 1
+//   k_goal_reset      warm encode: the previous goal cell is released as a free cell restarting at u = 0
+//                     (C7: a free cell at the maximum u = 1 would be a spurious maximum)
 //   k_track_predict   one thread per track, fp64: warp radius (Eq. 15 closed form, C16),
 //                     warp number t (C17), horizon j (Eq. 16, C18), j Kalman predicts
 //                     (Eqs. 9-10), footprint R^2 (C19-C20), bounding box
@@ -55,7 +56,7 @@ __device__ __forceinline__ void goal_reset_one(const EncodeArgs& e, const ScenPa
     if (sp.old_gx == sp.gx && sp.old_gy == sp.gy) return;
     const int b = sp.b;
     if (e.mask[((int64_t)b * e.H + sp.old_gy) * e.W + sp.old_gx]) return;
-    (sp.cur ? e.u1 : e.u0)[(int64_t)b * e.sstride + (int64_t)sp.old_gy * e.P + sp.old_gx] = -1.0f;  // free, u = 1
+    (sp.cur ? e.u1 : e.u0)[(int64_t)b * e.sstride + (int64_t)sp.old_gy * e.P + sp.old_gx] = -0.0f;  // free, u = 0
 }
 
 __device__ __forceinline__ void set_goal_one(const EncodeArgs& e, const ScenParams& sp) {

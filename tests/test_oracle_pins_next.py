@@ -284,11 +284,18 @@ def test_p25_resample_and_next_waypoint_by_hand(orc):
 
 # --------------------------------------------------------------------- P26 (C7 warm start)
 def test_p26_warm_init_by_hand(orc):
-    # C7: free cells keep the previous value, including cells fixed last tick and free now;
+    # C7: free cells keep the previous value, including a cell that was an obstacle last tick
+    # (u = 0); a released goal restarts at u = 0 like a released obstacle (it must not stay a free
+    # cell at the maximum u = 1: that is a spurious maximum, the descent-walk trap C7 avoids);
     # fixed cells take their class value (goal 1, obstacle 0)
     prev = np.array([[0.375, 0.0, 1.0], [0.75, 0.25, 0.125]], np.float32)
+    cls_prev = np.array([[0, 1, 2], [0, 0, 0]], np.uint8)
     cls = np.array([[0, 0, 0], [1, 2, 0]], np.uint8)   # the old obstacle (0,1) and goal (0,2) are free now
-    u = orc.init_u32(cls, prev)
-    assert u.tolist() == [[0.375, 0.0, 1.0], [0.0, 1.0, 0.125]]
+    u = orc.init_u32(cls, prev, cls_prev)
+    assert u.tolist() == [[0.375, 0.0, 0.0], [0.0, 1.0, 0.125]]
+    # without the previous class grid nothing is known to be released: every free cell keeps its value
+    assert orc.init_u32(cls, prev).tolist() == [[0.375, 0.0, 1.0], [0.0, 1.0, 0.125]]
+    # a goal that stays put is re-fixed at 1
+    assert orc.init_u32(cls_prev, prev, cls_prev).tolist() == [[0.375, 0.0, 1.0], [0.75, 0.25, 0.125]]
     # cold: free 0.5
     assert orc.init_u32(cls).tolist() == [[0.5, 0.5, 0.5], [0.0, 1.0, 0.5]]
