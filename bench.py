@@ -63,6 +63,7 @@ def _args():
     ap.add_argument("--batch", type=int, default=1024, help="c5: total scenarios")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the c4_slab / c5_batch sub-results")
     ap.add_argument("--probe", action="store_true", help="launcher check: every rank prints its rank and exits")
     return ap.parse_args()
 
@@ -314,6 +315,11 @@ def run_ours(args):
         "prep": prep,
         "clocks": clocks,
     }
+    if not args.no_sub:
+        # the two configurations that shard, measured in the same job at the same N so
+        # that the driver's 1/2/4/8 runs carry their scaling too
+        out["c4_slab"] = c4_slab(args, dev, ws, rank, local)
+        out["c5_batch"] = c5_batch(args, dev, ws, rank, local)
     if rank == 0 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
@@ -329,9 +335,57 @@ def run_ours(args):
 
 
 # ---------------------------------------------------------------------------- C4: row slabs
+def c4_slab(args, dev, ws, rank, local):
+    """16384^2 relaxation, rows split over the ranks as libtwg sharded contexts (twg_create with an
+    NCCL communicator): inside twg_relax the library exchanges the 2k ghost rows every k sweeps
+    (ncclSend/ncclRecv on a high-priority stream, overlapped with the interior tiles) and
+    max-all-reduces the residual on the device.  Strong scaling.  Returns the sub-result dict."""
+    import torch
+    from paper_1903_07441_b200 import relax_cfg, warp_cfg
+    from paper_1903_07441_b200.slab import make_sharded, nccl_comm_for
+    from paper_1903_07441_b200.twg import nccl_comm_destroy
+    from scenes import scene_c4
+    sc = scene_c4(0)
+    stream = torch.cuda.current_stream(dev)
+    comm = nccl_comm_for(rank, ws, local)
+    pl = make_sharded(sc.W, sc.H, sc.static, sc.robot, sc.goal, sc.tracks, warp_cfg(), args.k, comm, device=local,
+                      stream=stream.cuda_stream)
+    S = args.relax_sweeps
+    rc = relax_cfg(max_sweeps=S, temporal_depth=args.T, rows_per_warp=args.rows)
+    for _ in range(args.warmup):
+        pl.relax(rc, want_result=False)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = pl.kernel_launches()
+    e0.record(stream)
+    for _ in range(args.steps):
+        pl.relax(rc, want_result=False)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_tot = e0.elapsed_time(e1)
+    launches = pl.kernel_launches() - l0
+    _, res = pl.relax(relax_cfg(max_sweeps=args.k), want_result=True)
+    if ws > 1:
+        t = torch.tensor([ms_tot], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_tot = float(t.item())
+    out = {"metric": "harmonic relaxation GLUP/s at 16384^2 (row slabs)", "unit": "GLUP/s",
+           "value": sc.W * sc.H * S * args.steps / (ms_tot * 1e-3) / 1e9, "scaling": "strong", "n_gpus": ws,
+           "ms_per_step": ms_tot / args.steps, "steps": args.steps,
+           "config": {"workload": f"c4_16384: {sc.W}x{sc.H} grid, {sc.n_tracks} obstacles, relax {S} red-black "
+                                  f"sweeps per step, ghost exchange every k={args.k} sweeps inside twg_relax "
+                                  f"(NCCL send/recv; residual all-reduce)",
+                      "k": args.k, "ghost_rows": pl.ghost_rows, "rows_per_rank": pl.r1 - pl.r0,
+                      "l2": "not flushed: the 16384^2 field (1 GiB, 2 GiB ping-pong) exceeds L2"},
+           "gpu_launches": int(launches), "residual_after": float(res[0])}
+    pl.close()
+    nccl_comm_destroy(comm)
+    return out
+
+
 def run_c4(args):
-    """16384^2 relaxation, rows split over the ranks, 2k ghost rows exchanged every k sweeps
-    (NCCL point-to-point), residual max-all-reduced at the end.  Strong scaling."""
     import torch
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
@@ -339,75 +393,26 @@ def run_c4(args):
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    from paper_1903_07441_b200 import warp_cfg, lib
-    from paper_1903_07441_b200.slab import SlabLayout, SlabRelaxer, TwgSlabBackend, DistExchanger, make_twg_slab
-    from scenes import scene_c4
+    from paper_1903_07441_b200 import lib
     lib()
-    sc = scene_c4(0)
-    lay = SlabLayout(sc.W, sc.H, ws, rank, args.k)
-    stream = torch.cuda.current_stream(dev)
-    pl = make_twg_slab(lay, sc.static, sc.robot, sc.goal, sc.tracks, warp_cfg(), device=local, stream=stream.cuda_stream)
-    be = TwgSlabBackend(pl, local)
-
-    class _Single:  # world size 1: nothing to exchange
-        def exchange(self, lay, field):
-            pass
-
-        def allreduce_max(self, v, device=None):
-            return v
-
-    relaxer = SlabRelaxer(be, lay, DistExchanger() if ws > 1 else _Single(), device=dev)
-    S = args.relax_sweeps
-    for _ in range(args.warmup):
-        relaxer.relax(S)
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ms_tot = 0.0
-    l0 = pl.kernel_launches()
     with Clocks(local, enabled=not args.no_clocks) as clk:
-        for _ in range(args.steps):
-            e0.record(stream)
-            s, res = relaxer.relax(S)
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
-            ms_tot += e0.elapsed_time(e1)
-    launches = pl.kernel_launches() - l0
-    if ws > 1:
-        t = torch.tensor([ms_tot], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_tot = float(t.item())
-    value = sc.W * sc.H * S * args.steps / (ms_tot * 1e-3) / 1e9
+        out = c4_slab(args, dev, ws, rank, local)
     if rank == 0:
-        print(json.dumps({"metric": "harmonic relaxation GLUP/s at 16384^2 (row slabs)", "value": value, "unit": UNIT,
-                          "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_tot / args.steps,
-                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                          "data": "synthetic",
-                          "config": {"workload": f"c4_16384: {sc.W}x{sc.H} grid, {sc.n_tracks} obstacles, relax "
-                                                 f"{S} sweeps per step, ghost exchange every k={args.k} sweeps",
-                                     "k": args.k, "ghost_rows": lay.G, "rows_per_rank": lay.r1 - lay.r0,
-                                     "l2": "not flushed: the 16384^2 field (1 GiB, 2 GiB ping-pong) exceeds L2"},
-                          "gpu_launches": int(launches), "residual": res, "clocks": clk.summary()}), flush=True)
-    pl.close()
+        out.update({"warmup": args.warmup, "higher_is_better": True, "vs_baseline": None, "dtype": "f32",
+                    "data": "synthetic", "clocks": clk.summary()})
+        print(json.dumps(out), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------- C5: batch
-def run_c5(args):
+def c5_batch(args, dev, ws, rank, local):
     """1024 independent 512^2 scenarios, 1024/N per rank in one batched context (weak in the
-    scenarios per rank).  A step = twg_plan_step(b = -1) with S = 100 warm sweeps."""
+    scenarios per rank).  A step = twg_plan_step(b = -1) with S = 100 warm sweeps.  Returns the
+    sub-result dict."""
     import torch
-    ws, rank, local = _dist()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    from paper_1903_07441_b200 import Planner, band_cfg, relax_cfg, warp_cfg, lib
+    from paper_1903_07441_b200 import Planner, band_cfg, relax_cfg, warp_cfg
     from scenes import scene_random, advance_scene
-    lib()
     per = args.batch // ws
     scs = [scene_random(f"c5_s{s}", 512, 8, 20, s) for s in range(rank * per, (rank + 1) * per)]
     stream = torch.cuda.current_stream(dev)
@@ -415,7 +420,6 @@ def run_c5(args):
     for b, sc in enumerate(scs):
         pl.set_static(sc.static, b)
     wc, bc = warp_cfg(), band_cfg(args.band_iters, 4096, 8192)
-
     ticks = {}
 
     def inputs(tick):  # scene advance and packing are input generation: done before the timed region
@@ -432,7 +436,6 @@ def run_c5(args):
 
     for k in range(1 + args.warmup + args.steps):
         inputs(k)
-
     t_prep = time.perf_counter()
     step(0, relax_cfg(max_sweeps=100000, check_every=2000, tol=1e-38, warm_start=0, sync_every=4))
     prep_s = time.perf_counter() - t_prep
@@ -443,17 +446,21 @@ def run_c5(args):
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     ms_tot, ok = 0.0, 0
+    status = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local, enabled=not args.no_clocks) as clk:
-        for k in range(args.steps):
-            torch.cuda.nvtx.range_push("timed_region")
-            e0.record(stream)
-            st, res, _, _ = step(1 + args.warmup + k, rc)
-            torch.cuda.nvtx.range_pop()
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
-            ms_tot += e0.elapsed_time(e1)
-            ok += sum(1 for r in res if r.walk_status == 0)
+    l0 = pl.kernel_launches()
+    for k in range(args.steps):
+        torch.cuda.nvtx.range_push("timed_region")
+        e0.record(stream)
+        st, res, _, _ = step(1 + args.warmup + k, rc)
+        e1.record(stream)
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize(dev)
+        ms_tot += e0.elapsed_time(e1)
+        ok += sum(1 for r in res if r.walk_status == 0)
+        for r in res:
+            status[int(r.status)] = status.get(int(r.status), 0) + 1
+    launches = pl.kernel_launches() - l0
     gathered = per
     if ws > 1:
         t = torch.tensor([ms_tot], device=dev, dtype=torch.float64)
@@ -469,20 +476,35 @@ def run_c5(args):
         okt = torch.tensor([ok], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(okt)
         ok = int(okt.item())
-    value = 512 * 512 * per * ws * args.sweeps * args.steps / (ms_tot * 1e-3) / 1e9
-    if rank == 0:
-        print(json.dumps({"metric": "harmonic relaxation GLUP/s, batch of 512^2 plan steps", "value": value,
-                          "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-                          "ms_per_step": ms_tot / args.steps, "higher_is_better": True, "scaling": "weak",
-                          "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                          "config": {"workload": f"c5: {args.batch} x 512x512 scenarios (20 obstacles each), "
-                                                 f"{per} per rank, warm plan step S={args.sweeps}, "
-                                                 f"I={args.band_iters} (host tracks include per-step H2D)"},
-                          "scenario_steps_per_s": per * ws * args.steps / (ms_tot * 1e-3),
-                          "walk_ok_fraction": ok / (args.steps * per * ws), "prep_s": prep_s,
-                          "results_gathered": gathered,
-                          "clocks": clk.summary()}), flush=True)
+    out = {"metric": "harmonic relaxation GLUP/s, batch of 512^2 plan steps", "unit": "GLUP/s",
+           "value": 512 * 512 * per * ws * args.sweeps * args.steps / (ms_tot * 1e-3) / 1e9, "scaling": "weak",
+           "n_gpus": ws, "ms_per_step": ms_tot / args.steps, "steps": args.steps,
+           "config": {"workload": f"c5: {args.batch} x 512x512 scenarios (20 obstacles each), {per} per rank, "
+                                  f"warm plan step S={args.sweeps}, I={args.band_iters} (host tracks: per-step H2D "
+                                  f"inside the timed region)"},
+           "scenario_steps_per_s": per * ws * args.steps / (ms_tot * 1e-3),
+           "walk_ok_fraction": ok / (args.steps * per * ws), "status_counts_rank0": status, "prep_s": prep_s,
+           "results_gathered": gathered, "gpu_launches": int(launches)}
     pl.close()
+    return out
+
+
+def run_c5(args):
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1903_07441_b200 import lib
+    lib()
+    with Clocks(local, enabled=not args.no_clocks) as clk:
+        out = c5_batch(args, dev, ws, rank, local)
+    if rank == 0:
+        out.update({"warmup": args.warmup, "higher_is_better": True, "vs_baseline": None, "dtype": "f32",
+                    "data": "synthetic", "clocks": clk.summary()})
+        print(json.dumps(out), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 

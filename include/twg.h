@@ -75,17 +75,27 @@ enum {
 /* Grid of `batch` independent scenarios of width x height cells of
  * cell_size metres (0.1 m), cell (0,0)'s corner at (origin_x,
  * origin_y).
- * Row slabs: row_offset = global index of local row
- * 0, so the red/black colour is the parity of (x + row_offset + y) (C1);
- * ghost_rows = G rows at the top and at the bottom of the local grid that are
- * copies of the neighbouring slabs (owned rows are [G, height - G)).  With
- * G > 0 the residual of twg_relax covers the owned rows only, the goal and the
- * robot may lie outside the local grid (their cells are then simply absent),
- * and twg_extract_path / twg_plan_step are not available.  Single-GPU
- * contexts pass 0 and 0. */
+ * Row slabs come in two forms:
+ *  - sharded contexts (twg_create with an NCCL communicator, or
+ *    twg_create_group): the desc is the GLOBAL grid (batch 1, row_offset 0,
+ *    ghost_rows 0) and exchange_every = k >= 1 sweeps between ghost
+ *    exchanges; the library gives slab r of n the owned global rows
+ *    [r0, r1) = [r H/n, (r + 1) H/n) (near-equal split) plus G = 2k ghost rows
+ *    per side, exchanges them inside twg_relax and max-reduces the residual
+ *    across slabs on the device (twg_slab_info reports the geometry);
+ *  - manual slabs (no communicator): row_offset = global index of local row
+ *    0, so the red/black colour is the parity of (x + row_offset + y) (C1);
+ *    ghost_rows = G rows at the top and at the bottom of the local grid that
+ *    the caller keeps as copies of the neighbouring slabs (owned rows are
+ *    [G, height - G)).
+ * With G > 0 the residual of twg_relax covers the owned rows only, the goal
+ * and the robot may lie outside the local grid (their cells are then simply
+ * absent), and twg_extract_path / twg_plan_step are not available (the walk
+ * is handed over between slabs with twg_walk_from).  Single-GPU contexts pass
+ * 0 for row_offset, ghost_rows and exchange_every. */
 typedef struct {
     int32_t width, height, batch, row_offset;
-    int32_t ghost_rows, reserved;
+    int32_t ghost_rows, exchange_every;
     double cell_size, origin_x, origin_y;
 } twg_grid_desc;
 
@@ -216,14 +226,54 @@ typedef struct {
  * stream).  Allocates 2 ping-pong fields of height x pitch fp32 per scenario
  * (pitch = width rounded up to 32) plus a uint8 static mask.  Every field
  * starts as all-free cold (u = 0.5) with no goal.
- * Errors: INVALID_ARG (sizes <= 0, cell_size <= 0, batch > 65535), CUDA, NO_MEMORY. */
-TWG_API twg_status twg_create(const twg_grid_desc* desc, int32_t device, void* cuda_stream, twg_ctx** out);
+ * nccl_comm: NULL = single GPU (or a manual slab); else an ncclComm_t (from
+ * twg_nccl_comm_init, or any communicator of the same libnccl.so.2, e.g.
+ * torch's ProcessGroupNCCL._comm_ptr()) whose rank r of n makes this context
+ * slab r of the global grid `desc` (row slabs; see
+ * twg_grid_desc).  Every rank must then call twg_relax with the same
+ * configuration: the ghost rows are exchanged with ncclSend / ncclRecv every
+ * exchange_every sweeps on a high-priority stream, overlapped with the
+ * interior tiles, and the residual is max-all-reduced (ncclAllReduce) before
+ * the stop rule is evaluated on the device.  The communicator is borrowed: it
+ * must outlive the context.
+ * Errors: INVALID_ARG (sizes <= 0, cell_size <= 0, batch > 65535; slabs: batch
+ * != 1, exchange_every < 1, a slab thinner than 2 exchange_every rows), CUDA,
+ * NCCL, NO_MEMORY. */
+TWG_API twg_status twg_create(const twg_grid_desc* desc, int32_t device, void* cuda_stream, void* nccl_comm,
+                              twg_ctx** out);
+
+/* nslabs (1..16) row-slab contexts of the global grid `desc` on one device,
+ * out[nslabs] in slab order (a local group: the row-slab decomposition of
+ * twg_create with a communicator, with ghost rows exchanged by device copies
+ * instead of NCCL).  twg_relax on any member relaxes the whole
+ * group (sweeps_done / residual are the group's).  Destroy every member;
+ * destroying one detaches the others (they then act as manual slabs).
+ * Errors as twg_create. */
+TWG_API twg_status twg_create_group(const twg_grid_desc* desc, int32_t nslabs, int32_t device, void* cuda_stream,
+                                    twg_ctx** out);
+
+/* Slab geometry of ctx: out8 = {rank, nranks, r0, r1 (owned global rows
+ * [r0, r1)), row_offset (global row of local row 0), ghost_rows,
+ * exchange_every, local height}.  Unsharded: {0, 1, ...}. */
+TWG_API twg_status twg_slab_info(const twg_ctx* ctx, int32_t* out8);
+
+/* NCCL communicator helpers for sharded contexts (the library resolves NCCL
+ * at run time from the libnccl.so.2 the process has loaded, e.g. torch's).
+ * twg_nccl_unique_id: ncclGetUniqueId into out (bytes >= 128; broadcast it to
+ * every rank, e.g. with torch.distributed); twg_nccl_comm_init:
+ * ncclCommInitRank on `device` (collective over the nranks ranks);
+ * twg_nccl_comm_destroy: ncclCommDestroy.  Errors: INVALID_ARG, NCCL, CUDA. */
+TWG_API twg_status twg_nccl_unique_id(void* out, int32_t bytes);
+TWG_API twg_status twg_nccl_comm_init(int32_t nranks, const void* id, int32_t rank, int32_t device, void** comm);
+TWG_API twg_status twg_nccl_comm_destroy(void* comm);
 
 /* Release all device memory of the context.  NULL is a no-op. */
 TWG_API twg_status twg_destroy(twg_ctx* ctx);
 
 /* Static wall mask of scenario b (b = -1: every scenario), height x width
  * uint8 row-major, non-zero = wall ("phi(x,y) = 1"; P:586 red lines).
+ * Sharded contexts take the GLOBAL mask and keep their local rows (rows
+ * outside the global grid are walls, C4).
  * Host or device pointer.  The next twg_set_obstacles re-encodes cold. */
 TWG_API twg_status twg_set_static(twg_ctx* ctx, int32_t b, const uint8_t* occ);
 
@@ -235,6 +285,7 @@ TWG_API twg_status twg_set_static(twg_ctx* ctx, int32_t b, const uint8_t* occ);
  *   a3 field encode: cells whose centre lies within R of a predicted
  *      position become obstacles, static walls stay obstacles, the goal cell
  *      is the goal, the robot's cell stays free (C22).
+ * Sharded contexts take the goal in global cells.
  * warm = 0: every free cell restarts at 0.5 ("cleared");
  * warm = 1: every free cell keeps the value it holds, including cells fixed
  * in the previous call and free now (a released obstacle keeps u = 0), except

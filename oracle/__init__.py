@@ -35,7 +35,7 @@ OK, W_GOAL_SWALLOWED, E_INVALID_ARG, E_OUT_OF_BOUNDS, E_OVERLAPPING, E_INVALID_S
 def build(force: bool = False) -> str:
     """Compile the oracle (no FMA contraction, no fast-math, no FTZ/DAZ)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
                "-Wall", "-o", _LIB, _SRC, "-lm"]
         subprocess.check_call(cmd)
     return _LIB
@@ -97,6 +97,10 @@ def lib():
         L.orc_init_u64.argtypes = [i64, P, P]
         L.orc_relax_f32.restype = i32
         L.orc_relax_f32.argtypes = [i32, i32, P, P, i32, i32, f32, P]
+        L.orc_relax_f32_omp.restype = i32
+        L.orc_relax_f32_omp.argtypes = [i32, i32, P, P, i32, i32, f32, i32, P]
+        L.orc_band_omp.restype = None
+        L.orc_band_omp.argtypes = [i32, i32, P, P, i32, P, i32, f32, f32, i32]
         L.orc_relax_f32_ex.restype = i32
         L.orc_relax_f32_ex.argtypes = [i32, i32, P, P, i32, i32, f32, i32, i32, i32, P]
         L.orc_relax_f64.restype = i32
@@ -210,13 +214,23 @@ def init_u64(cls):
 
 
 # ---------------------------------------------------------------- O4, O5
-def relax_f32(cls, u, max_sweeps, check_every=1, tol=0.0):
-    """In-place red-black relaxation of float32 u.  Returns (sweeps, residual)."""
+def host_cores():
+    """Host cores this process may use (the OpenMP timing variants' default thread count)."""
+    return len(os.sched_getaffinity(0))
+
+
+def relax_f32(cls, u, max_sweeps, check_every=1, tol=0.0, threads=1):
+    """In-place red-black relaxation of float32 u.  Returns (sweeps, residual).  threads > 1: the
+    OpenMP variant (bit-identical, P14)."""
     assert u.dtype == np.float32 and u.flags.c_contiguous
     cls = np.ascontiguousarray(cls, np.uint8)
     H, W = u.shape
     r = np.zeros(1, np.float32)
-    s = lib().orc_relax_f32(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol), _p(r))
+    if threads > 1:
+        s = lib().orc_relax_f32_omp(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol),
+                                    int(threads), _p(r))
+    else:
+        s = lib().orc_relax_f32(W, H, _p(cls), _p(u), int(max_sweeps), int(check_every), float(tol), _p(r))
     return int(s), float(r[0])
 
 
@@ -348,12 +362,16 @@ def bilerp(u, px, py):
     return lib().orc_bilerp(W, H, _p(u), float(px), float(py))
 
 
-def band(cls, u, waypoints, iters=50, step=0.25, kt=1.0):
+def band(cls, u, waypoints, iters=50, step=0.25, kt=1.0, threads=1):
     cls = np.ascontiguousarray(cls, np.uint8)
     u = np.ascontiguousarray(u, np.float32)
     H, W = u.shape
     w = np.ascontiguousarray(waypoints, np.float32).reshape(-1, 2).copy()
-    lib().orc_band(W, H, _p(cls), _p(u), w.shape[0], _p(w), int(iters), np.float32(step), np.float32(kt))
+    if threads > 1:
+        lib().orc_band_omp(W, H, _p(cls), _p(u), w.shape[0], _p(w), int(iters), np.float32(step), np.float32(kt),
+                           int(threads))
+    else:
+        lib().orc_band(W, H, _p(cls), _p(u), w.shape[0], _p(w), int(iters), np.float32(step), np.float32(kt))
     return w
 
 
@@ -379,7 +397,7 @@ def next_waypoint(pts):
 
 
 def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0.25, kt=1.0,
-              max_len=None, prev=None, jacobi=False, horizon_mode=0, footprint_mode=0, lex=False):
+              max_len=None, prev=None, jacobi=False, horizon_mode=0, footprint_mode=0, lex=False, threads=1):
     """One planning tick, Algorithm 1 on the CPU.
 
     prev: None (cold start) or the dict returned by the previous call (warm
@@ -393,15 +411,18 @@ def plan_step(scene, max_sweeps=100, check_every=None, tol=0.0, iters=50, step=0
         u = init_u32(cls)
     else:
         u = init_u32(cls, prev["u"], prev.get("cls"))
-    relax = relax_jacobi_f32 if jacobi else (relax_lex_f32 if lex else relax_f32)
-    sweeps, res = relax(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol)
+    if jacobi or lex:
+        relax = relax_jacobi_f32 if jacobi else relax_lex_f32
+        sweeps, res = relax(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol)
+    else:
+        sweeps, res = relax_f32(cls, u, max_sweeps, check_every or max(max_sweeps, 1), tol, threads=threads)
     if max_len is None:
         max_len = 4 * (scene.W + scene.H)
     wst, cells = walk(cls, u, robot_cell(scene), max_len)
     out = {"status": st, "cls": cls, "u": u, "t": t, "j": j, "pred": pred, "sweeps": sweeps,
            "residual": res, "walk_status": wst, "cells": cells}
     if wst == OK:
-        w = band(cls, u, cells_to_waypoints(cells), iters, step, kt)
+        w = band(cls, u, cells_to_waypoints(cells), iters, step, kt, threads=threads)
         sm, _ = resample(w)
         k, nx, ny = next_waypoint(sm)
         out.update(band=w, smooth=sm, next=(nx, ny))

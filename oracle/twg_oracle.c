@@ -324,6 +324,42 @@ int32_t orc_relax_f32(int32_t W, int32_t H, const uint8_t* cls, float* u,
     return orc_relax_f32_ex(W, H, cls, u, max_sweeps, check_every, tol, 0, 0, H, res_out);
 }
 
+/* orc_relax_f32 with each colour pass split over `threads` OpenMP threads by rows (timing variant,
+ * SURVEY 8(c)).  The cells of one colour never neighbour each other, so within a pass every update
+ * reads only the other colour and the pass is order-free; the residual is a max, which is exact in
+ * any order.  Hence the result is bit-identical to the single-thread loop (pin P14). */
+int32_t orc_relax_f32_omp(int32_t W, int32_t H, const uint8_t* cls, float* u, int32_t max_sweeps,
+                          int32_t check_every, float tol, int32_t threads, float* res_out)
+{
+    float res = 0.0f;
+    int32_t s = 0;
+    if (check_every < 1) check_every = 1;
+    if (threads < 1) threads = 1;
+    for (s = 1; s <= max_sweeps; ++s) {
+        res = 0.0f;
+        for (int color = 0; color < 2; ++color) {
+#pragma omp parallel for num_threads(threads) schedule(static) reduction(max : res)
+            for (int32_t y = 0; y < H; ++y)
+                for (int32_t x = (color + y) & 1; x < W; x += 2) {
+                    size_t q = (size_t)y * W + x;
+                    if (cls[q] != ORC_FREE) continue;
+                    float uE = x + 1 < W ? u[q + 1] : 0.0f;
+                    float uW = x > 0 ? u[q - 1] : 0.0f;
+                    float uN = y > 0 ? u[q - W] : 0.0f;
+                    float uS = y + 1 < H ? u[q + W] : 0.0f;
+                    float nv = 0.25f * ((uE + uW) + (uN + uS));
+                    float d = fabsf(nv - u[q]);
+                    if (d > res) res = d;
+                    u[q] = nv;
+                }
+        }
+        if ((s % check_every == 0 && res < tol) || s == max_sweeps) break;
+    }
+    if (max_sweeps <= 0) { s = 0; res = 0.0f; }
+    if (res_out) *res_out = res;
+    return s;
+}
+
 int32_t orc_relax_f64(int32_t W, int32_t H, const uint8_t* cls, double* u,
                       int32_t max_sweeps, int32_t check_every, double tol, double* res_out)
 {
@@ -610,6 +646,24 @@ void orc_band(int32_t W, int32_t H, const uint8_t* cls, const float* u,
                 orc_band_point(W, H, cls, u, w + 2 * (i - 1), w + 2 * i, w + 2 * (i + 1), step, kt, o);
                 w[2 * i] = o[0]; w[2 * i + 1] = o[1];
             }
+}
+
+/* orc_band with each parity phase split over `threads` OpenMP threads (timing variant): the
+ * waypoints of one parity read only waypoints of the other parity, so a phase is order-free and
+ * the result is bit-identical to orc_band (pin P14). */
+void orc_band_omp(int32_t W, int32_t H, const uint8_t* cls, const float* u,
+                  int32_t n, float* w, int32_t iters, float step, float kt, int32_t threads)
+{
+    if (threads < 1) threads = 1;
+    for (int32_t it = 0; it < iters; ++it)
+        for (int p = 1; p >= 0; --p) {
+#pragma omp parallel for num_threads(threads) schedule(static)
+            for (int32_t i = 1 + (p == 0); i < n - 1; i += 2) {
+                float o[2];
+                orc_band_point(W, H, cls, u, w + 2 * (i - 1), w + 2 * i, w + 2 * (i + 1), step, kt, o);
+                w[2 * i] = o[0]; w[2 * i + 1] = o[1];
+            }
+        }
 }
 
 /* Resample (C15): each segment of length l is replaced by

@@ -8,7 +8,7 @@ import sys
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_HERE)
 SOURCES = ["api.cu", "api_track.cu", "api_sim.cu", "api_extra.cu", "host_core.cu", "k_relax.cu", "k_stamp.cu",
-           "k_path.cu", "k_track.cu", "k_sim.cu"]
+           "k_path.cu", "k_track.cu", "k_sim.cu", "nccl_link.cu"]
 HEADERS = ["twg_internal.cuh", "twg_kernels.cuh", "api_host.cuh"]
 OUT = os.path.join(_HERE, "libtwg.so")
 
@@ -16,6 +16,9 @@ OUT = os.path.join(_HERE, "libtwg.so")
 # default IEEE division/sqrt and no flush-to-zero (no --use_fast_math).
 NVCC_FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-fmad=false",
               "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared"]
+
+
+LINK_LIBS = ["-ldl"]
 
 
 def _nvcc():
@@ -34,13 +37,32 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit in parallel (one nvcc per file), then link libtwg.so."""
     if not force and not needs_build():
         return OUT
-    srcs = [os.path.join(_HERE, "csrc", s) for s in SOURCES]
-    cmd = [_nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include")] + srcs + ["-o", OUT + ".tmp"]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
+    inc = ["-I", os.path.join(ROOT, "include")]
+    comp = [f for f in NVCC_FLAGS if f != "-shared"]
+    with tempfile.TemporaryDirectory(prefix="twg_build_") as tmp:
+        objs = [os.path.join(tmp, os.path.splitext(s)[0] + ".o") for s in SOURCES]
+
+        def one(k):
+            cmd = [_nvcc()] + comp + inc + ["-c", os.path.join(_HERE, "csrc", SOURCES[k]), "-o", objs[k]]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed on {SOURCES[k]}:\n{r.stdout}{r.stderr}")
+            if r.stderr.strip() and verbose:
+                print(r.stderr, file=sys.stderr)
+
+        with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+            list(ex.map(one, range(len(SOURCES))))
+        cmd = [_nvcc()] + NVCC_FLAGS + objs + LINK_LIBS + ["-o", OUT + ".tmp"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

@@ -14,8 +14,8 @@ using namespace twg::host;
 
 
 // =====================================================================================
-TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stream, twg_ctx** out) {
-    if (!d || !out) return fail(nullptr, TWG_E_INVALID_ARG, "null argument");
+// Allocate and initialise a context for the local grid `d` (unsharded, or one slab).
+static twg_status create_local(const twg_grid_desc* d, int32_t device, void* stream, twg_ctx** out) {
     *out = nullptr;
     if (d->width <= 0 || d->height <= 0 || d->batch <= 0 || !(d->cell_size > 0.0))
         return fail(nullptr, TWG_E_INVALID_ARG, "width, height, batch > 0 and cell_size > 0 required");
@@ -95,10 +95,128 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
     return TWG_OK;
 }
 
+// Comm stream (highest priority) and join events of a row-slab context or local group.
+struct SlabStreams {
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    ~SlabStreams() {
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        if (comm) cudaStreamDestroy(comm);
+    }
+};
+
+static twg_status make_streams(std::shared_ptr<void>* out) {
+    auto s = std::make_shared<SlabStreams>();
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaError_t e = cudaStreamCreateWithPriority(&s->comm, cudaStreamNonBlocking, hi);
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&s->ev[k], cudaEventDisableTiming);
+    if (e != cudaSuccess) return fail(nullptr, TWG_E_CUDA, std::string("slab streams: ") + cudaGetErrorString(e));
+    *out = s;
+    return TWG_OK;
+}
+
+static void attach_streams(twg_ctx* c, const std::shared_ptr<void>& s) {
+    const SlabStreams* ss = static_cast<const SlabStreams*>(s.get());
+    c->shard.streams = s;
+    c->shard.comm = ss->comm;
+    for (int k = 0; k < 3; ++k) c->shard.ev[k] = ss->ev[k];
+}
+
+// Slab `rank` of `nranks` of the global grid d: owned global rows [r0, r1) (near-equal
+// contiguous split) plus G = 2k ghost rows per side, local row 0 = global row r0 - G.
+static twg_status create_slab(const twg_grid_desc* d, int rank, int nranks, int32_t device, void* stream,
+                              twg_ctx** out) {
+    const int k = d->exchange_every;
+    if (k < 1) return fail(nullptr, TWG_E_INVALID_ARG, "a row-slab context needs exchange_every >= 1");
+    if (d->batch != 1 || d->ghost_rows != 0 || d->row_offset != 0)
+        return fail(nullptr, TWG_E_INVALID_ARG, "row slabs: batch 1, ghost_rows 0 and row_offset 0 in the global desc");
+    const int G = 2 * k;
+    const int base = d->height / nranks, extra = d->height % nranks;
+    const int r0 = rank * base + std::min(rank, extra);
+    const int r1 = r0 + base + (rank < extra ? 1 : 0);
+    if (r1 - r0 < G) return fail(nullptr, TWG_E_INVALID_ARG, "slab thinner than 2 exchange_every rows");
+    twg_grid_desc l = *d;
+    l.height = r1 - r0 + 2 * G;
+    l.row_offset = r0 - G;
+    l.ghost_rows = G;
+    l.origin_y = d->origin_y + (double)(r0 - G) * d->cell_size;
+    twg_status st = create_local(&l, device, stream, out);
+    if (st != TWG_OK) return st;
+    twg_ctx* c = *out;
+    c->shard.nranks = nranks;
+    c->shard.rank = rank;
+    c->shard.k = k;
+    c->shard.H_global = d->height;
+    c->shard.r0 = r0;
+    c->shard.r1 = r1;
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stream, void* nccl_comm, twg_ctx** out) {
+    if (!d || !out) return fail(nullptr, TWG_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    if (!nccl_comm) return create_local(d, device, stream, out);
+    int rank = 0, nranks = 1;
+    twg_status st = nccl_comm_rank(nullptr, nccl_comm, &rank, &nranks);
+    if (st != TWG_OK) return st;
+    std::shared_ptr<void> ss;
+    st = make_streams(&ss);
+    if (st != TWG_OK) return st;
+    st = create_slab(d, rank, nranks, device, stream, out);
+    if (st != TWG_OK) return st;
+    (*out)->shard.nccl = nccl_comm;
+    attach_streams(*out, ss);
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_create_group(const twg_grid_desc* d, int32_t nslabs, int32_t device, void* stream,
+                                    twg_ctx** out) {
+    if (!d || !out || nslabs < 1 || nslabs > kMaxLocalSlabs)
+        return fail(nullptr, TWG_E_INVALID_ARG, "null argument or nslabs outside 1..16");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(nullptr, TWG_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    std::shared_ptr<void> ss;
+    twg_status st = make_streams(&ss);
+    if (st != TWG_OK) return st;
+    std::vector<twg_ctx*> g(nslabs, nullptr);
+    for (int r = 0; r < nslabs; ++r) {
+        st = create_slab(d, r, nslabs, device, stream, &g[r]);
+        if (st != TWG_OK) {
+            for (twg_ctx* c : g) twg_destroy(c);
+            return st;
+        }
+        attach_streams(g[r], ss);
+    }
+    for (int r = 0; r < nslabs; ++r) {
+        g[r]->shard.peers = g;
+        out[r] = g[r];
+    }
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_slab_info(const twg_ctx* c, int32_t* out8) {
+    if (!c || !out8) return TWG_E_INVALID_ARG;
+    const bool sh = c->sharded();
+    out8[0] = sh ? c->shard.rank : 0;
+    out8[1] = sh ? c->shard.nranks : 1;
+    out8[2] = sh ? c->shard.r0 : c->row_off + c->ghost;
+    out8[3] = sh ? c->shard.r1 : c->row_off + c->H - c->ghost;
+    out8[4] = c->row_off;
+    out8[5] = c->ghost;
+    out8[6] = sh ? c->shard.k : 0;
+    out8[7] = c->H;
+    return TWG_OK;
+}
+
 TWG_API twg_status twg_destroy(twg_ctx* c) {
     if (!c) return TWG_OK;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    // a slab leaving its local group breaks the group: the other slabs forget their peers
+    for (twg_ctx* p : c->shard.peers)
+        if (p != c) p->shard.peers.clear();
     void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_ctl,   c->d_meta,   c->d_tracks,   c->d_t,
                     c->d_j,      c->d_pred,    c->d_boxes, c->d_param_block, c->d_track_off, c->d_cells, c->d_wp,
                     c->d_smooth, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
@@ -122,6 +240,21 @@ TWG_API twg_status twg_set_static(twg_ctx* c, int32_t b, const uint8_t* occ) {
     const size_t n = (size_t)c->H * c->W;
     const bool dev = is_device_ptr(occ);
     const int b0 = b < 0 ? 0 : b, b1 = b < 0 ? c->B : b + 1;
+    if (c->sharded()) {
+        // occ is the global H_global x W mask: take the local rows, rows outside the grid are walls (C4)
+        const size_t W = c->W;
+        for (int y = 0; y < c->H; ++y) {
+            const int gy = c->row_off + y;
+            uint8_t* dst = c->hmask.data() + (size_t)y * W;
+            if (gy < 0 || gy >= c->shard.H_global) std::memset(dst, 1, W);
+            else if (dev) TWG_CUDA(c, cudaMemcpy(dst, occ + (size_t)gy * W, W, cudaMemcpyDeviceToHost));
+            else std::memcpy(dst, occ + (size_t)gy * W, W);
+        }
+        TWG_CUDA(c, cudaMemcpyAsync(c->mask, c->hmask.data(), n, cudaMemcpyHostToDevice, c->stream));
+        c->scen[0].static_dirty = true;
+        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+        return TWG_OK;
+    }
     for (int q = b0; q < b1; ++q) {
         if (dev) {
             TWG_CUDA(c, cudaMemcpyAsync(c->mask + q * n, occ, n, cudaMemcpyDeviceToDevice, c->stream));
@@ -143,6 +276,7 @@ TWG_API twg_status twg_set_obstacles(twg_ctx* c, int32_t b, const twg_robot* rob
     if (!robot || b < 0 || b >= c->B || (n > 0 && !tracks)) return fail(c, TWG_E_INVALID_ARG, "bad argument");
     const bool resident = !tracks && n == TWG_RESIDENT_TRACKS;
     if (resident) n = c->scen[b].trk_n;
+    if (c->sharded()) goal_y -= c->row_off;  // global goal row -> local
     EncodeReq r{b, *robot, goal_x, goal_y, n, 0};
     st = encode(c, {r}, tracks, cfg, warm, resident);
     if (st != TWG_OK) return st;

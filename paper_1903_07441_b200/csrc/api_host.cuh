@@ -47,9 +47,22 @@ twg_status validate(twg_ctx* c, const EncodeReq& r, int* rcx, int* rcy);
 // Rows a1-a3 for a list of scenarios (resident: use the tracker tables already in d_tracks).
 twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_track* tracks, const twg_warp_cfg* wc,
                   int warm_req, bool resident = false);
-// Rows a4-a6 for the scenarios with part[b] != 0.
+// Rows a4-a6 for the scenarios with part[b] != 0 (a context of a local slab group relaxes the group).
 twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& part, int* sweeps_done,
                  float* residual);
+twg_status relax_group(const std::vector<twg_ctx*>& g, const twg_relax_cfg* cfg, const std::vector<int>& part,
+                       int* sweeps_done, float* residual);
+
+// NCCL (nccl_link.cu): resolved at run time from the libnccl.so.2 already loaded by the process
+// (torch's), else loaded by name; every call reports TWG_E_NCCL through fail() on error.
+twg_status nccl_load(twg_ctx* c);
+twg_status nccl_comm_rank(twg_ctx* c, void* comm, int* rank, int* nranks);
+// One group call: send s_up (cnt floats) to `up` and receive r_up from it, the same with `dn`
+// (-1: no such neighbour).
+twg_status nccl_exchange(twg_ctx* c, size_t cnt, int up, int dn, const float* s_up, float* r_up, const float* s_dn,
+                         float* r_dn, cudaStream_t st);
+twg_status nccl_allreduce_max_u32(twg_ctx* c, unsigned* buf, int n, cudaStream_t st);
+twg_status nccl_bcast_i32(twg_ctx* c, int* buf, int n, int root, cudaStream_t st);
 // Rows a7-a9 for a list of scenarios (results stay on the device).
 twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg);
 // Row f1 tick for the requests rq (det_off relative to `det`, a device array of (x, y) pairs).

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -428,182 +429,356 @@ twg_status ensure_lex(twg_ctx* c) {
     return TWG_OK;
 }
 
-// Rows a4-a6 for the scenarios whose participation flag is set: launches of T sweeps (red-black),
-// single sweeps (Jacobi) or persistent launches (lexicographic), then k_check per check interval.
-twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& part, int* sweeps_done,
-                 float* residual) {
-    if (!cfg) return fail(c, TWG_E_INVALID_ARG, "null relax cfg");
+// ---------------------------------------------------------------- rows a4-a6
+// One red-black tile launch of t sweeps over output rows [lo, hi) of every participating scenario
+// of c.  The colour parity of row lo is folded into the kernel's compile-time parity (QOFF).
+static twg_status launch_rb_range(twg_ctx* c, const twg_relax_cfg* cfg, int t, int lp, int lo, int hi, bool resid,
+                                  int nscen, cudaStream_t st) {
+    RelaxArgs a;
+    a.u0 = c->u[0];
+    a.u1 = c->u[1];
+    a.cur = c->d_cur;
+    a.P = c->P;
+    a.sstride = c->sstride;
+    a.W = c->W;
+    a.H = c->H;
+    a.done = c->d_done;
+    a.res = c->d_res_bits;
+    a.res_r0 = c->ghost;
+    a.res_r1 = c->H - c->ghost;
+    a.lp = lp & 1;
+    a.row_lo = lo;
+    a.row_hi = hi;
+    a.n_strips = (c->W + out_cols(t) - 1) / out_cols(t);
+    a.hseg = auto_hseg(t, hi - lo, a.n_strips, std::max(nscen, 1), cfg->rows_per_warp, c->n_sm);
+    a.seg_begin = 0;
+    a.seg_end = (hi - lo + a.hseg - 1) / a.hseg;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    const bool prof = c->prof && st == c->stream;
+    if (prof) {
+        while ((int)c->ev_pool.size() < c->ev_used + 2) {
+            cudaEvent_t ev;
+            TWG_CUDA(c, cudaEventCreate(&ev));
+            c->ev_pool.push_back(ev);
+        }
+        e0 = c->ev_pool[c->ev_used++];
+        e1 = c->ev_pool[c->ev_used++];
+        TWG_CUDA(c, cudaEventRecord(e0, st));
+    }
+    TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0][t], c->tmap[1][t], a, c->B, (c->row_off + lo) & 1, resid, st));
+    if (prof) {
+        TWG_CUDA(c, cudaEventRecord(e1, st));
+        c->prof_launches += 1;
+        c->prof_cells += (int64_t)nscen * c->W * (hi - lo) * t;
+    }
+    c->launches += 1;
+    return TWG_OK;
+}
+
+// `to` waits for everything enqueued on `from` so far.
+static twg_status join(twg_ctx* c, cudaStream_t from, cudaStream_t to, int slot) {
+    if (from == to) return TWG_OK;
+    cudaEvent_t e = c->shard.ev[slot];
+    TWG_CUDA(c, cudaEventRecord(e, from));
+    TWG_CUDA(c, cudaStreamWaitEvent(to, e, 0));
+    return TWG_OK;
+}
+
+// Buffer holding scenario 0's field after `lp` launches of the current call.
+static float* cur_field(twg_ctx* c, int lp) { return c->u[c->cur[0] ^ (lp & 1)]; }
+
+// Ghost-row exchange of a row-slab group: every slab sends its G = 2k owned boundary
+// rows to each neighbour and receives the neighbour's into its ghost rows.  NCCL point-to-point
+// (one group call per rank) or, for a local group, device copies; enqueued on the comm stream.
+static twg_status exchange(const std::vector<twg_ctx*>& g, int lp) {
+    twg_ctx* c0 = g[0];
+    cudaStream_t cs = c0->shard.comm;
+    const int G = c0->ghost;
+    if (c0->shard.nccl) {
+        twg_ctx* c = c0;
+        const size_t cnt = (size_t)G * c->P;
+        float* f = cur_field(c, lp);
+        const int r = c->shard.rank, n = c->shard.nranks;
+        if (n == 1) return TWG_OK;
+        return nccl_exchange(c, cnt, r > 0 ? r - 1 : -1, r + 1 < n ? r + 1 : -1, f + (size_t)G * c->P, f,
+                             f + (size_t)(c->H - 2 * G) * c->P, f + (size_t)(c->H - G) * c->P, cs);
+    }
+    for (size_t r = 0; r + 1 < g.size(); ++r) {
+        twg_ctx* up = g[r];
+        twg_ctx* dn = g[r + 1];
+        float* fu = cur_field(up, lp);
+        float* fd = cur_field(dn, lp);
+        const size_t bytes = (size_t)G * up->P * sizeof(float);
+        // up's owned bottom rows -> dn's top ghosts; dn's owned top rows -> up's bottom ghosts
+        TWG_CUDA(c0, cudaMemcpyAsync(fd, fu + (size_t)(up->H - 2 * G) * up->P, bytes, cudaMemcpyDeviceToDevice, cs));
+        TWG_CUDA(c0, cudaMemcpyAsync(fu + (size_t)(up->H - G) * up->P, fd + (size_t)G * dn->P, bytes,
+                                     cudaMemcpyDeviceToDevice, cs));
+    }
+    return TWG_OK;
+}
+
+// Residual max over the slabs of a group (residual bits of the owned rows; floats >= 0 order as
+// their bit patterns), enqueued on the comm stream: NCCL all-reduce(max) or a one-block kernel.
+static twg_status residual_max(const std::vector<twg_ctx*>& g) {
+    twg_ctx* c0 = g[0];
+    if (c0->shard.nccl) {
+        if (c0->shard.nranks == 1) return TWG_OK;
+        return nccl_allreduce_max_u32(c0, c0->d_res_bits, c0->B, c0->shard.comm);
+    }
+    if (g.size() < 2) return TWG_OK;
+    unsigned* ptrs[kMaxLocalSlabs];
+    for (size_t r = 0; r < g.size(); ++r) ptrs[r] = g[r]->d_res_bits;
+    TWG_CUDA(c0, launch_res_group_max(ptrs, (int)g.size(), c0->B, c0->shard.comm));
+    c0->launches += 1;
+    return TWG_OK;
+}
+
+// Rows a4-a6 for the scenarios whose participation flag is set, on one context or on a row-slab
+// group (all slabs of one process: the local group, or this rank's slab of an NCCL group).
+// Launches of T sweeps (red-black), single sweeps (Jacobi) or persistent launches (lexicographic),
+// then k_check per check interval.  Row slabs run the check interval as exchange
+// intervals of at most k sweeps: the j-th launch of an interval writes only the rows still valid
+// after it (the ghost region shrinks by 2T rows per launch), the last launch of an interval is split
+// into the two boundary bands (comm stream) and the interior (context stream), so that the ghost
+// exchange of the boundary rows overlaps the interior tiles; the residual is max-reduced across
+// slabs on the device before k_check, so every slab applies the same stop rule without a host hop.
+twg_status relax_group(const std::vector<twg_ctx*>& g, const twg_relax_cfg* cfg, const std::vector<int>& part,
+                       int* sweeps_done, float* residual) {
+    twg_ctx* c0 = g[0];
+    if (!cfg) return fail(c0, TWG_E_INVALID_ARG, "null relax cfg");
     const int maxs = cfg->max_sweeps;
-    if (maxs < 0 || cfg->check_every < 0) return fail(c, TWG_E_INVALID_ARG, "negative sweep counts");
-    if (cfg->mode < 0 || cfg->mode > 2) return fail(c, TWG_E_INVALID_ARG, "relax mode must be 0, 1 or 2");
+    if (maxs < 0 || cfg->check_every < 0) return fail(c0, TWG_E_INVALID_ARG, "negative sweep counts");
+    if (cfg->mode < 0 || cfg->mode > 2) return fail(c0, TWG_E_INVALID_ARG, "relax mode must be 0, 1 or 2");
     const bool jacobi = cfg->mode == 1;
     const bool lex = cfg->mode == 2;
-    if (lex && c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "lexicographic mode is not available on a row slab");
+    const bool sh = c0->sharded();
+    if (lex && c0->ghost > 0) return fail(c0, TWG_E_INVALID_ARG, "lexicographic mode is not available on a row slab");
     if (lex) {
-        twg_status ls = ensure_lex(c);
+        twg_status ls = ensure_lex(c0);
         if (ls != TWG_OK) return ls;
     }
-    const int B = c->B;
+    const int B = c0->B;
     int T = cfg->temporal_depth > 0 ? std::min(cfg->temporal_depth, kMaxT) : 6;
     const float tol = cfg->tol;
     int check = (tol > 0.0f && cfg->check_every > 0) ? cfg->check_every : std::max(maxs, 1);
     const int sync_every = cfg->sync_every > 0 ? cfg->sync_every : 64;
+    const int kx = sh ? c0->shard.k : std::numeric_limits<int>::max();  // sweeps between exchanges
+    cudaStream_t ms = c0->stream, cs = sh ? c0->shard.comm : c0->stream;
     // control arrays [done | cur | sweeps | where | res bits | res]: when the buffer indices or the
     // participation changed since the last call, one copy of the whole block; otherwise a kernel
     // resets done / sweeps / where / residual, so consecutive relaxations stay a chain of kernels
-    // (PDL included) -- the row-slab intervals
-    bool all = true;
-    for (int b = 0; b < B; ++b) all = all && part[b];
-    bool same = (int)c->cur_cache.size() == B && (int)c->part_cache.size() == B;
-    for (int b = 0; same && b < B; ++b) same = c->cur_cache[b] == c->cur[b] && c->part_cache[b] == (part[b] ? 1 : 0);
-    if (!same || !all) {
-        int* hs = nullptr;
-        TWG_CUDA(c, stage_alloc(c, 6 * B * sizeof(int), reinterpret_cast<void**>(&hs)));
-        c->cur_cache.assign(B, 0);
-        c->part_cache.assign(B, 0);
-        for (int b = 0; b < B; ++b) {
-            hs[b] = part[b] ? 0 : 1;
-            hs[B + b] = c->cur_cache[b] = c->cur[b];
-            c->part_cache[b] = part[b] ? 1 : 0;
-            hs[2 * B + b] = 0;
-            hs[3 * B + b] = -1;
-            hs[4 * B + b] = 0;
-            hs[5 * B + b] = 0;  // +0.0f
-        }
-        TWG_CUDA(c, cudaMemcpyAsync(c->d_ctl, hs, 6 * B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    } else {
-        TWG_CUDA(c, launch_relax_init(c->d_done, c->d_sweeps, c->d_where, c->d_res_bits, c->d_res, B, c->stream));
-        c->launches += 1;
-    }
-    if (lex)
-        TWG_CUDA(c, cudaMemsetAsync(c->d_lex_tdone, 0, (size_t)B * c->lex_tx * c->lex_ty * sizeof(int), c->stream));
+    // (PDL included)
     int nscen = 0;
     for (int b = 0; b < B; ++b) nscen += part[b] ? 1 : 0;
+    for (twg_ctx* c : g) {
+        bool all = true;
+        for (int b = 0; b < B; ++b) all = all && part[b];
+        bool same = (int)c->cur_cache.size() == B && (int)c->part_cache.size() == B;
+        for (int b = 0; same && b < B; ++b) same = c->cur_cache[b] == c->cur[b] && c->part_cache[b] == (part[b] ? 1 : 0);
+        if (!same || !all) {
+            int* hs = nullptr;
+            TWG_CUDA(c, stage_alloc(c, 6 * B * sizeof(int), reinterpret_cast<void**>(&hs)));
+            c->cur_cache.assign(B, 0);
+            c->part_cache.assign(B, 0);
+            for (int b = 0; b < B; ++b) {
+                hs[b] = part[b] ? 0 : 1;
+                hs[B + b] = c->cur_cache[b] = c->cur[b];
+                c->part_cache[b] = part[b] ? 1 : 0;
+                hs[2 * B + b] = 0;
+                hs[3 * B + b] = -1;
+                hs[4 * B + b] = 0;
+                hs[5 * B + b] = 0;  // +0.0f
+            }
+            TWG_CUDA(c, cudaMemcpyAsync(c->d_ctl, hs, 6 * B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        } else {
+            TWG_CUDA(c, launch_relax_init(c->d_done, c->d_sweeps, c->d_where, c->d_res_bits, c->d_res, B, c->stream));
+            c->launches += 1;
+        }
+    }
+    if (lex)
+        TWG_CUDA(c0, cudaMemsetAsync(c0->d_lex_tdone, 0, (size_t)B * c0->lex_tx * c0->lex_ty * sizeof(int), ms));
 
     int lp = 0;  // launches so far (parity)
     if (maxs > 0) {
-        RelaxArgs a;
-        a.u0 = c->u[0];
-        a.u1 = c->u[1];
-        a.cur = c->d_cur;
-        a.P = c->P;
-        a.sstride = c->sstride;
-        a.W = c->W;
-        a.H = c->H;
-        a.done = c->d_done;
-        a.res = c->d_res_bits;
-        a.res_r0 = c->ghost;
-        a.res_r1 = c->H - c->ghost;
-        const int qoff = c->row_off & 1;
         int done_sw = 0, nchunk = 0;
         int lex_base = 0;  // sweeps finished by earlier lexicographic launches of this call
         while (done_sw < maxs) {
             const int chunk = std::min(check, maxs - done_sw);
-            // launches of T sweeps, then the remainder; the last launch accumulates the residual (the
-            // tracking costs the most in the deepest kernel, so a short remainder launch carries it)
-            std::vector<int> plan;
-            if (jacobi) {
-                plan.assign(chunk, 1);
-            } else if (lex) {
-                for (int q = 0; q < chunk / kLexMaxSweeps; ++q) plan.push_back(kLexMaxSweeps);  // persistent launches
-                if (chunk % kLexMaxSweeps) plan.push_back(chunk % kLexMaxSweeps);
-            } else {
-                for (int q = 0; q < chunk / T; ++q) plan.push_back(T);
-                if (chunk % T) plan.push_back(chunk % T);
-            }
-            for (size_t q = 0; q < plan.size(); ++q) {
-                const int t = plan[q];
-                a.n_strips = (c->W + out_cols(t) - 1) / out_cols(t);
-                a.hseg = auto_hseg(t, c->H, a.n_strips, std::max(nscen, 1), cfg->rows_per_warp, c->n_sm);
-                a.seg_begin = 0;
-                a.seg_end = (c->H + a.hseg - 1) / a.hseg;
-                a.lp = lp & 1;
-                cudaEvent_t e0 = nullptr, e1 = nullptr;
-                if (c->prof) {
-                    while ((int)c->ev_pool.size() < c->ev_used + 2) {
-                        cudaEvent_t ev;
-                        TWG_CUDA(c, cudaEventCreate(&ev));
-                        c->ev_pool.push_back(ev);
+            for (int in_chunk = 0; in_chunk < chunk;) {
+                const int n = std::min(kx, chunk - in_chunk);  // one exchange interval
+                const bool resid_iv = in_chunk + n == chunk;    // the chunk's last sweep is in this interval
+                // launches of T sweeps, then the remainder; the last launch accumulates the residual
+                std::vector<int> plan;
+                if (jacobi) {
+                    plan.assign(n, 1);
+                } else if (lex) {
+                    for (int q = 0; q < n / kLexMaxSweeps; ++q) plan.push_back(kLexMaxSweeps);  // persistent launches
+                    if (n % kLexMaxSweeps) plan.push_back(n % kLexMaxSweeps);
+                } else {
+                    for (int q = 0; q < n / T; ++q) plan.push_back(T);
+                    if (n % T) plan.push_back(n % T);
+                }
+                int s = 0;  // sweeps of this interval done after the launch
+                // the last launch of the interval is split when every slab is thick enough (the two
+                // boundary bands [lo, 2G) and [H - 2G, hi) and a non-empty interior)
+                bool split = sh && !jacobi && !lex;
+                for (twg_ctx* c : g) split = split && c->ghost > 0 && c->H - 2 * n - 2 * n >= 4 * c->ghost + 2;
+                bool split_done = false;
+                for (size_t q = 0; q < plan.size(); ++q) {
+                    const int t = plan[q];
+                    s += t;
+                    const bool lastl = q + 1 == plan.size();
+                    const bool resid = resid_iv && lastl;
+                    if (lex) {
+                        int2* tl = lex_tasks(c0, t);
+                        if (!tl) return fail(c0, TWG_E_NO_MEMORY, "lexicographic task list");
+                        LexArgs la;
+                        la.u0 = c0->u[0];
+                        la.u1 = c0->u[1];
+                        la.cur = c0->d_cur;
+                        la.P = c0->P;
+                        la.sstride = c0->sstride;
+                        la.W = c0->W;
+                        la.H = c0->H;
+                        la.B = B;
+                        la.TX = c0->lex_tx;
+                        la.TY = c0->lex_ty;
+                        la.ntiles = c0->lex_tx * c0->lex_ty;
+                        la.tasks = tl;
+                        la.ntasks = t * c0->lex_tx * c0->lex_ty;
+                        la.sweeps = t;
+                        la.base = lex_base;
+                        lex_base += t;
+                        la.tdone = c0->d_lex_tdone;
+                        la.task = c0->d_lex_task;
+                        la.done = c0->d_done;
+                        la.res = resid ? c0->d_res_bits : nullptr;  // the chunk's last sweep only
+                        la.res_r0 = c0->ghost;
+                        la.res_r1 = c0->H - c0->ghost;
+                        TWG_CUDA(c0, cudaMemsetAsync(c0->d_lex_task, 0, sizeof(unsigned), ms));
+                        TWG_CUDA(c0, launch_lex(la, c0->n_sm, ms));
+                        c0->launches += 1;
+                        continue;  // the lexicographic sweep is in place (no parity change)
                     }
-                    e0 = c->ev_pool[c->ev_used++];
-                    e1 = c->ev_pool[c->ev_used++];
-                    TWG_CUDA(c, cudaEventRecord(e0, c->stream));
+                    for (twg_ctx* c : g) {
+                        if (jacobi) {
+                            RelaxArgs a;
+                            std::memset(&a, 0, sizeof(a));
+                            a.u0 = c->u[0];
+                            a.u1 = c->u[1];
+                            a.cur = c->d_cur;
+                            a.P = c->P;
+                            a.sstride = c->sstride;
+                            a.W = c->W;
+                            a.H = c->H;
+                            a.done = c->d_done;
+                            a.res = c->d_res_bits;
+                            a.res_r0 = c->ghost;
+                            a.res_r1 = c->H - c->ghost;
+                            a.lp = lp & 1;
+                            TWG_CUDA(c, launch_jacobi(a, B, resid, c->stream));
+                            c->launches += 1;
+                            continue;
+                        }
+                        // rows valid after s sweeps of the interval: all but 2s at each edge of a slab
+                        const int lo = sh ? 2 * s : 0, hi = sh ? c->H - 2 * s : c->H;
+                        const int G = c->ghost;
+                        if (split && lastl) {
+                            // boundary bands first on the comm stream (the exchange reads them), the
+                            // interior on the context stream
+                            if (c == g[0]) {
+                                twg_status js = join(c0, ms, cs, 0);
+                                if (js != TWG_OK) return js;
+                            }
+                            twg_status r1 = launch_rb_range(c, cfg, t, lp, lo, 2 * G, resid, nscen, cs);
+                            if (r1 != TWG_OK) return r1;
+                            r1 = launch_rb_range(c, cfg, t, lp, c->H - 2 * G, hi, resid, nscen, cs);
+                            if (r1 != TWG_OK) return r1;
+                            r1 = launch_rb_range(c, cfg, t, lp, 2 * G, c->H - 2 * G, resid, nscen, ms);
+                            if (r1 != TWG_OK) return r1;
+                            split_done = true;
+                        } else {
+                            twg_status r1 = launch_rb_range(c, cfg, t, lp, lo, hi, resid, nscen, ms);
+                            if (r1 != TWG_OK) return r1;
+                        }
+                    }
+                    ++lp;
                 }
-                if (lex) {
-                    int2* tl = lex_tasks(c, t);
-                    if (!tl) return fail(c, TWG_E_NO_MEMORY, "lexicographic task list");
-                    LexArgs la;
-                    la.u0 = c->u[0];
-                    la.u1 = c->u[1];
-                    la.cur = c->d_cur;
-                    la.P = c->P;
-                    la.sstride = c->sstride;
-                    la.W = c->W;
-                    la.H = c->H;
-                    la.B = B;
-                    la.TX = c->lex_tx;
-                    la.TY = c->lex_ty;
-                    la.ntiles = c->lex_tx * c->lex_ty;
-                    la.tasks = tl;
-                    la.ntasks = t * c->lex_tx * c->lex_ty;
-                    la.sweeps = t;
-                    la.base = lex_base;
-                    lex_base += t;
-                    la.tdone = c->d_lex_tdone;
-                    la.task = c->d_lex_task;
-                    la.done = c->d_done;
-                    la.res = q + 1 == plan.size() ? c->d_res_bits : nullptr;  // the chunk's last sweep only
-                    la.res_r0 = c->ghost;
-                    la.res_r1 = c->H - c->ghost;
-                    TWG_CUDA(c, cudaMemsetAsync(c->d_lex_task, 0, sizeof(unsigned), c->stream));
-                    TWG_CUDA(c, launch_lex(la, c->n_sm, c->stream));
-                } else if (jacobi)
-                    TWG_CUDA(c, launch_jacobi(a, B, q + 1 == plan.size(), c->stream));
-                else
-                    TWG_CUDA(c, launch_rb_tblock(t, c->tmap[0][t], c->tmap[1][t], a, B, qoff, q + 1 == plan.size(),
-                                                 c->stream));
-                if (c->prof) {
-                    TWG_CUDA(c, cudaEventRecord(e1, c->stream));
-                    c->prof_launches += 1;
-                    c->prof_cells += (int64_t)nscen * c->W * c->H * t;
+                if (sh) {
+                    // ghost exchange after every interval (the last one too: ghosts then hold the
+                    // neighbours' final rows for the slab walk); the boundary rows were written on
+                    // the comm stream when the last launch was split, otherwise wait for the launch
+                    if (!split_done) {
+                        twg_status js = join(c0, ms, cs, 0);
+                        if (js != TWG_OK) return js;
+                    }
+                    twg_status xs = exchange(g, lp);
+                    if (xs != TWG_OK) return xs;
+                    if (resid_iv) {
+                        twg_status js = join(c0, ms, cs, 1);  // the interior's residual
+                        if (js != TWG_OK) return js;
+                        twg_status rs = residual_max(g);
+                        if (rs != TWG_OK) return rs;
+                    }
+                    twg_status js = join(c0, cs, ms, 2);
+                    if (js != TWG_OK) return js;
                 }
-                c->launches += 1;
-                if (!lex) ++lp;  // the lexicographic sweep is in place
+                in_chunk += n;
             }
-            TWG_CUDA(c, launch_check(B, c->d_done, c->d_sweeps, c->d_res_bits, c->d_res, c->d_where, chunk, check, maxs,
-                                     tol, c->d_cur, lp & 1, c->stream));
-            c->launches += 1;
+            for (twg_ctx* c : g) {
+                TWG_CUDA(c, launch_check(B, c->d_done, c->d_sweeps, c->d_res_bits, c->d_res, c->d_where, chunk, check,
+                                         maxs, tol, c->d_cur, lp & 1, c->stream));
+                c->launches += 1;
+            }
             done_sw += chunk;
             ++nchunk;
             if (tol > 0.0f && done_sw < maxs && nchunk % sync_every == 0) {
+                // every slab took the same decision (reduced residual): reading slab 0 suffices
                 int* hd = nullptr;
-                TWG_CUDA(c, stage_alloc(c, B * sizeof(int), reinterpret_cast<void**>(&hd)));
-                TWG_CUDA(c, cudaMemcpyAsync(hd, c->d_done, B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-                TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+                TWG_CUDA(c0, stage_alloc(c0, B * sizeof(int), reinterpret_cast<void**>(&hd)));
+                TWG_CUDA(c0, cudaMemcpyAsync(hd, c0->d_done, B * sizeof(int), cudaMemcpyDeviceToHost, ms));
+                TWG_CUDA(c0, cudaStreamSynchronize(ms));
                 bool all = true;
                 for (int b = 0; b < B; ++b) all = all && hd[b];
                 if (all) break;
             }
         }
         if (tol > 0.0f) {  // only an early stop can leave a field in the other buffer
-            TWG_CUDA(c, launch_fixup(c->u[0], c->u[1], c->sstride, B, c->d_where, c->d_cur, lp & 1, c->stream));
-            c->launches += 1;
+            for (twg_ctx* c : g) {
+                TWG_CUDA(c, launch_fixup(c->u[0], c->u[1], c->sstride, B, c->d_where, c->d_cur, lp & 1, c->stream));
+                c->launches += 1;
+            }
+            if (sh) {  // the fixup moved whole fields: refresh the ghosts from the final owned rows
+                twg_status js = join(c0, ms, cs, 0);
+                if (js != TWG_OK) return js;
+                twg_status xs = exchange(g, lp);
+                if (xs != TWG_OK) return xs;
+                js = join(c0, cs, ms, 2);
+                if (js != TWG_OK) return js;
+            }
         }
-        for (int b = 0; b < B; ++b)
-            if (part[b]) c->cur[b] ^= (lp & 1);
+        for (twg_ctx* c : g)
+            for (int b = 0; b < B; ++b)
+                if (part[b]) c->cur[b] ^= (lp & 1);
     }
     if (sweeps_done || residual) {
         int* hsw = nullptr;  // [sweeps | where | res bits | res] in one copy
-        TWG_CUDA(c, stage_alloc(c, 4 * B * sizeof(int), reinterpret_cast<void**>(&hsw)));
+        TWG_CUDA(c0, stage_alloc(c0, 4 * B * sizeof(int), reinterpret_cast<void**>(&hsw)));
         float* hr = reinterpret_cast<float*>(hsw + 3 * B);
-        TWG_CUDA(c, cudaMemcpyAsync(hsw, c->d_sweeps, 4 * B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+        TWG_CUDA(c0, cudaMemcpyAsync(hsw, c0->d_sweeps, 4 * B * sizeof(int), cudaMemcpyDeviceToHost, ms));
+        TWG_CUDA(c0, cudaStreamSynchronize(ms));
         for (int b = 0; b < B; ++b) {
             if (sweeps_done) sweeps_done[b] = hsw[b];
             if (residual) residual[b] = hr[b];
         }
     }
     return TWG_OK;
+}
+
+twg_status relax(twg_ctx* c, const twg_relax_cfg* cfg, const std::vector<int>& part, int* sweeps_done,
+                 float* residual) {
+    if (!c->shard.peers.empty()) return relax_group(c->shard.peers, cfg, part, sweeps_done, residual);
+    return relax_group({c}, cfg, part, sweeps_done, residual);
 }
 
 // Rows a7-a9 for a list of scenarios (path kernels only; results stay on device).

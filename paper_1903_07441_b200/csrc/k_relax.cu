@@ -128,9 +128,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     const CUtensorMap* tmap = src ? &tmap1 : &tmap0;
 
     const int xb = strip * WOUT - HX;  // first (halo) column of the strip, even
-    const int y0 = seg * a.hseg;       // first output row, even
+    const int y0 = a.row_lo + seg * a.hseg;  // first output row (its parity is folded into QOFF)
     Strip st;
-    const int hs = min(a.hseg, a.H - y0);
+    const int hs = min(a.hseg, a.row_hi - y0);
     st.hs = (unsigned)hs;
     st.rlo = max(0, a.res_r0 - y0);
     st.rn = (unsigned)max(0, min(hs, a.res_r1 - y0) - st.rlo);
@@ -393,6 +393,27 @@ cudaError_t launch_relax_init(int* done, int* sweeps, int* where, unsigned* res_
     return cudaGetLastError();
 }
 
+// Residual max over the slabs of a local row-slab group: every slab's residual bits
+// become the group maximum (non-negative floats order as their bit patterns).
+struct GroupRes {
+    unsigned* p[kMaxLocalSlabs];
+};
+__global__ void k_res_group_max(GroupRes g, int n, int B) {
+    pdl_enter();
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        unsigned m = 0u;
+        for (int r = 0; r < n; ++r) m = max(m, g.p[r][b]);
+        for (int r = 0; r < n; ++r) g.p[r][b] = m;
+    }
+}
+
+cudaError_t launch_res_group_max(unsigned* const* ptrs, int n, int B, cudaStream_t st) {
+    GroupRes g;
+    for (int r = 0; r < kMaxLocalSlabs; ++r) g.p[r] = r < n ? ptrs[r] : nullptr;
+    k_res_group_max<<<1, 256, 0, st>>>(g, n, B);
+    return cudaGetLastError();
+}
+
 // After a chunk of `chunk` sweeps whose last launch accumulated the residual:
 // sweeps += chunk; stop when (sweeps % check_every == 0 && res < tol) or
 // sweeps == max_sweeps (C6).  `where` records which ping-pong buffer
@@ -484,6 +505,7 @@ void preload_relax_kernels() {
     cudaFuncGetAttributes(&a, k_check);
     cudaFuncGetAttributes(&a, k_relax_init);
     cudaFuncGetAttributes(&a, k_fixup);
+    cudaFuncGetAttributes(&a, k_res_group_max);
     cudaGetLastError();
 }
 

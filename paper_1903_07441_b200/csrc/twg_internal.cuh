@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
@@ -25,6 +26,7 @@ constexpr int kWarpsPerCta = 4;
 constexpr int kStripW = 128;
 constexpr int kStages = 2;
 constexpr int kMaxT = 8;
+constexpr int kMaxLocalSlabs = 16;  // slabs of one local row-slab group
 
 __host__ __device__ constexpr int halo_cols(int T) { return 4 * ((2 * T + 3) / 4); }  // round_up(2T, 4)
 __host__ __device__ constexpr int out_cols(int T) { return kStripW - 2 * halo_cols(T); }
@@ -39,6 +41,7 @@ struct RelaxArgs {
     int W, H;
     int n_strips, hseg;
     int seg_begin, seg_end;  // launched segment range
+    int row_lo, row_hi;  // output rows of this launch: segment s covers [row_lo + s hseg, ...) within row_hi
     int res_r0, res_r1;  // rows whose cells count in the residual (owned rows of a slab)
     const int* done;     // per-scenario done flags
     unsigned* res;       // per-scenario residual (float bits, atomicMax), used when RESID
@@ -272,6 +275,18 @@ struct twg_ctx {
     void* h_stage = nullptr;
     size_t h_stage_bytes = 0;
     size_t stage_off = 0;
+    // row-slab sharding: this context holds slab `rank` of `nranks` of a global grid of
+    // H_global rows, owned global rows [r0, r1) plus ghost = 2k rows per side (row_off = r0 - 2k)
+    struct Shard {
+        int nranks = 1, rank = 0, k = 0;  // k: sweeps between ghost exchanges
+        int H_global = 0, r0 = 0, r1 = 0;
+        void* nccl = nullptr;             // ncclComm_t of an NCCL group (not owned)
+        std::vector<twg_ctx*> peers;      // local group (one process), rank order; empty otherwise
+        cudaStream_t comm = nullptr;      // boundary bands, exchange and residual max
+        cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+        std::shared_ptr<void> streams;    // owner of comm / ev (shared by the slabs of a local group)
+    } shard;
+    bool sharded() const { return shard.nccl != nullptr || !shard.peers.empty(); }
     // accounting
     int64_t launches = 0;
     bool prof = false;

@@ -189,6 +189,45 @@ def make_twg_slab(layout: SlabLayout, static_global, robot, goal, tracks, warp, 
     return pl
 
 
+def nccl_comm_for(rank: int, world: int, device: int, group=None) -> int:
+    """An NCCL communicator for the libtwg sharded contexts (twg_nccl_comm_init): rank 0 draws the
+    unique id (twg_nccl_unique_id) and torch.distributed broadcasts it (any backend)."""
+    import torch.distributed as dist
+    from .twg import nccl_comm_init, nccl_unique_id
+    obj = [nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0, group=group)
+    return nccl_comm_init(world, obj[0], rank, device)
+
+
+def make_sharded(W, H, static_global, robot, goal, tracks, warp, k, nccl_comm, cell_size=0.1, origin=(0.0, 0.0),
+                 device=0, stream=None):
+    """This rank's slab of the global grid as a libtwg sharded context (twg_create with nccl_comm): the
+    library exchanges the ghost rows and reduces the residual inside twg_relax.  Encoded cold."""
+    from .twg import Planner
+    pl = Planner(W, H, 1, cell_size, origin, device=device, stream=stream, nccl_comm=nccl_comm, exchange_every=k)
+    pl.set_static(np.ascontiguousarray(np.asarray(static_global, np.uint8)))
+    pl.set_obstacles(0, robot, goal, tracks, warp, warm=0)
+    return pl
+
+
+def make_group(W, H, nslabs, static_global, robot, goal, tracks, warp, k, cell_size=0.1, origin=(0.0, 0.0),
+               device=0, stream=None):
+    """nslabs slabs of one global grid on one device (twg_create_group), encoded cold."""
+    from .twg import Planner
+    pls = Planner.create_group(W, H, nslabs, k, cell_size, origin, device, stream)
+    for pl in pls:
+        pl.set_static(np.ascontiguousarray(np.asarray(static_global, np.uint8)))
+        pl.set_obstacles(0, robot, goal, tracks, warp, warm=0)
+    return pls
+
+
+def owned_rows(pl, mode=0):
+    """The owned rows [r0, r1) of a slab context's field (twg_get_field returns the local slab)."""
+    f = pl.get_field(0, mode)
+    return f[pl.ghost_rows:pl.H - pl.ghost_rows]
+
+
 def exchange_local(backends, layouts):
     """Ghost-row exchange between slabs held by one process (device-to-device copies)."""
     views = [b.field_view() for b in backends]

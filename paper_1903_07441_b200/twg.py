@@ -25,7 +25,7 @@ RESIDENT_TRACKS = -1
 
 class GridDesc(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("batch", C.c_int32), ("row_offset", C.c_int32),
-                ("ghost_rows", C.c_int32), ("reserved", C.c_int32),
+                ("ghost_rows", C.c_int32), ("exchange_every", C.c_int32),
                 ("cell_size", C.c_double), ("origin_x", C.c_double), ("origin_y", C.c_double)]
 
 
@@ -80,7 +80,12 @@ class PlanResult(C.Structure):
 # (name, restype, argtypes) for every symbol of include/twg.h
 _P = C.c_void_p
 SIGNATURES = [
-    ("twg_create", C.c_int32, [C.POINTER(GridDesc), C.c_int32, _P, C.POINTER(_P)]),
+    ("twg_create", C.c_int32, [C.POINTER(GridDesc), C.c_int32, _P, _P, C.POINTER(_P)]),
+    ("twg_create_group", C.c_int32, [C.POINTER(GridDesc), C.c_int32, C.c_int32, _P, _P]),
+    ("twg_slab_info", C.c_int32, [_P, _P]),
+    ("twg_nccl_unique_id", C.c_int32, [_P, C.c_int32]),
+    ("twg_nccl_comm_init", C.c_int32, [C.c_int32, _P, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    ("twg_nccl_comm_destroy", C.c_int32, [_P]),
     ("twg_destroy", C.c_int32, [_P]),
     ("twg_set_static", C.c_int32, [_P, C.c_int32, _P]),
     ("twg_set_obstacles", C.c_int32, [_P, C.c_int32, C.POINTER(Robot), C.c_int32, C.c_int32, _P, C.c_int32,
@@ -196,20 +201,70 @@ def tracks_array(tracks):
     return t
 
 
+def nccl_unique_id() -> bytes:
+    """twg_nccl_unique_id: 128 opaque bytes to broadcast to every rank."""
+    buf = (C.c_uint8 * 128)()
+    st = lib().twg_nccl_unique_id(buf, 128)
+    if st != OK:
+        raise TwgError(st, lib().twg_last_error(None).decode())
+    return bytes(buf)
+
+
+def nccl_comm_init(nranks: int, uid: bytes, rank: int, device: int) -> int:
+    """twg_nccl_comm_init: an ncclComm_t (as an integer handle) for `rank` of `nranks`."""
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    h = C.c_void_p()
+    st = lib().twg_nccl_comm_init(int(nranks), buf, int(rank), int(device), C.byref(h))
+    if st != OK:
+        raise TwgError(st, lib().twg_last_error(None).decode())
+    return h.value
+
+
+def nccl_comm_destroy(comm: int):
+    st = lib().twg_nccl_comm_destroy(C.c_void_p(comm))
+    if st != OK:
+        raise TwgError(st, lib().twg_last_error(None).decode())
+
+
 class Planner:
-    """Owns one twg_ctx.  Method names mirror the C ABI (twg_<name>)."""
+    """Owns one twg_ctx.  Method names mirror the C ABI (twg_<name>).
+
+    nccl_comm (an ncclComm_t handle, e.g. from :func:`nccl_comm_init`) with exchange_every = k makes
+    this context the caller's row slab of the global width x height grid (twg_create)."""
 
     def __init__(self, width, height, batch=1, cell_size=0.1, origin=(0.0, 0.0), device=0, stream=None,
-                 row_offset=0, ghost_rows=0):
-        self.W, self.H, self.B = int(width), int(height), int(batch)
-        self.row_offset, self.ghost_rows = int(row_offset), int(ghost_rows)
-        d = GridDesc(self.W, self.H, self.B, self.row_offset, self.ghost_rows, 0, float(cell_size),
-                     float(origin[0]), float(origin[1]))
-        h = C.c_void_p()
-        st = lib().twg_create(C.byref(d), int(device), stream, C.byref(h))
+                 row_offset=0, ghost_rows=0, nccl_comm=None, exchange_every=0, _ctx=None):
+        self.W, self.B = int(width), int(batch)
+        if _ctx is not None:  # a member of twg_create_group
+            self.ctx = _ctx
+        else:
+            d = GridDesc(self.W, int(height), self.B, int(row_offset), int(ghost_rows), int(exchange_every),
+                         float(cell_size), float(origin[0]), float(origin[1]))
+            h = C.c_void_p()
+            st = lib().twg_create(C.byref(d), int(device), stream, None if nccl_comm is None else C.c_void_p(nccl_comm),
+                                  C.byref(h))
+            if st != OK:
+                raise TwgError(st, lib().twg_last_error(None).decode())
+            self.ctx = h
+        info = self.slab_info()
+        self.rank, self.nranks, self.r0, self.r1 = info[0], info[1], info[2], info[3]
+        self.row_offset, self.ghost_rows, self.exchange_every, self.H = info[4], info[5], info[6], info[7]
+
+    @staticmethod
+    def create_group(width, height, nslabs, exchange_every, cell_size=0.1, origin=(0.0, 0.0), device=0, stream=None):
+        """twg_create_group: nslabs row-slab Planners of one global grid on one device (local group)."""
+        d = GridDesc(int(width), int(height), 1, 0, 0, int(exchange_every), float(cell_size), float(origin[0]),
+                     float(origin[1]))
+        hs = (C.c_void_p * int(nslabs))()
+        st = lib().twg_create_group(C.byref(d), int(nslabs), int(device), stream, hs)
         if st != OK:
             raise TwgError(st, lib().twg_last_error(None).decode())
-        self.ctx = h
+        return [Planner(width, 0, 1, _ctx=C.c_void_p(hs[r])) for r in range(int(nslabs))]
+
+    def slab_info(self):
+        out = np.zeros(8, np.int32)
+        _check(self.ctx, lib().twg_slab_info(self.ctx, _ptr(out)))
+        return [int(v) for v in out]
 
     def close(self):
         if self.ctx:

@@ -511,3 +511,28 @@ def test_p14_determinism(orc):
     b = orc.plan_step(sc, max_sweeps=60, iters=5)
     assert np.array_equal(a["u"], b["u"]) and np.array_equal(a["cls"], b["cls"])
     assert a["sweeps"] == b["sweeps"] == 60
+
+
+def test_p14_openmp_variants_bit_identical(orc):
+    # the OpenMP timing variants (colour passes / band parity phases split over
+    # threads) are bit-identical to the single-thread oracle -- same field, sweeps, residual, band
+    from scenes import scene_random
+    sc = scene_random("p14", 128, 3, 6, 8)  # a seed whose walk reaches the goal at tol 1e-7
+    threads = max(2, min(8, orc.host_cores()))
+    st, cls, *_ = orc.classify(sc)
+    u1 = orc.init_u32(cls)
+    u2 = u1.copy()
+    for S, ce, tol in ((37, 37, 0.0), (40000, 10, 1e-7)):
+        s1, r1 = orc.relax_f32(cls, u1, S, ce, tol)
+        s2, r2 = orc.relax_f32(cls, u2, S, ce, tol, threads=threads)
+        assert (s1, np.float32(r1)) == (s2, np.float32(r2))
+        assert np.array_equal(u1.view(np.uint32), u2.view(np.uint32))
+    wst, cells = orc.walk(cls, u1, orc.robot_cell(sc), 10000)
+    assert wst == 0
+    w0 = orc.cells_to_waypoints(cells)
+    b1 = orc.band(cls, u1, w0, 30)
+    b2 = orc.band(cls, u1, w0, 30, threads=threads)
+    assert np.array_equal(b1.view(np.uint32), b2.view(np.uint32))
+    p1 = orc.plan_step(sc, max_sweeps=50, iters=10)
+    p2 = orc.plan_step(sc, max_sweeps=50, iters=10, threads=threads)
+    assert np.array_equal(p1["u"], p2["u"]) and np.array_equal(p1["smooth"], p2["smooth"])
