@@ -141,8 +141,9 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------- CPU oracle arm
-def _oracle_sample(args, sweeps, steps, seed=0):
-    """Oracle plan steps (single thread, as it stands) on the same workload; GLUP/s."""
+def _oracle_sample(args, sweeps, steps, seed=0, threads=1):
+    """Oracle plan steps (as it stands; its OpenMP variants on `threads` host cores, bit-identical to
+    the single-thread oracle, P14) on the same workload; GLUP/s."""
     import oracle
     from scenes import advance_scene
     sc0 = _scene(args, seed)
@@ -151,7 +152,8 @@ def _oracle_sample(args, sweeps, steps, seed=0):
     for k in range(steps):
         sc = advance_scene(sc0, k)
         t0 = time.perf_counter()
-        prev = oracle.plan_step(sc, max_sweeps=sweeps, iters=args.band_iters, max_len=4 * (sc.W + sc.H), prev=prev)
+        prev = oracle.plan_step(sc, max_sweeps=sweeps, iters=args.band_iters, max_len=4 * (sc.W + sc.H), prev=prev,
+                                threads=threads)
         t_total += time.perf_counter() - t0
         lups += sc.W * sc.H * sweeps
     return lups / t_total / 1e9, t_total
@@ -163,17 +165,19 @@ def run_reference(args):
         return
     import oracle
     oracle.build()
-    s = max(1, min(args.sweeps, 25))
-    _oracle_sample(args, s, args.warmup)
-    g, t = _oracle_sample(args, s, args.steps)
+    s = args.sweeps  # the GPU arm's S: same workload, same metric
+    cores = oracle.host_cores()
+    _oracle_sample(args, s, args.warmup, threads=cores)
+    g, t = _oracle_sample(args, s, args.steps, threads=cores)
     line = {"metric": METRIC, "value": g, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": {"workload": f"c3_{args.size}: {args.size}x{args.size} grid, {args.obstacles} moving obstacles, "
                                    f"one plan step per step (oracle sample: S={s} sweeps, I={args.band_iters})",
                        "sweeps": s},
-            "cpu_baseline": {"value": g, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} oracle plan steps of c3 seed 0 with S={s} sweeps"},
+            "cpu_baseline": {"value": g, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} oracle plan steps of c3 seed 0 with S={s} sweeps, "
+                                       f"I={args.band_iters} (OpenMP variants on {cores} host cores)"},
             "e2e": {"value": g, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -323,10 +327,14 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
-        g, t = _oracle_sample(args, args.sweeps, 2)
-        out["cpu_baseline"] = {"value": g, "unit": UNIT, "cores": 1, "kind": "oracle",
-                               "sample": f"2 warm oracle plan steps of c3 seed 0 (S={args.sweeps}, "
-                                         f"I={args.band_iters}), {t:.1f} s, single thread"}
+        cores = oracle.host_cores()
+        g, t = _oracle_sample(args, args.sweeps, 3, threads=cores)
+        g1, t1 = _oracle_sample(args, args.sweeps, 1, threads=1)
+        out["cpu_baseline"] = {"value": g, "unit": UNIT, "cores": cores, "kind": "oracle",
+                               "sample": f"3 oracle plan steps of c3 seed 0 (cold, then warm; S={args.sweeps}, "
+                                         f"I={args.band_iters}), {t:.1f} s, OpenMP variants on {cores} host cores "
+                                         f"(bit-identical to the single-thread oracle, P14)",
+                               "single_thread": {"value": g1, "cores": 1, "sample": f"1 plan step, {t1:.1f} s"}}
     if rank == 0:
         print(json.dumps(out), flush=True)
     pl.close()

@@ -597,6 +597,20 @@ twg_status relax_group(const std::vector<twg_ctx*>& g, const twg_relax_cfg* cfg,
     }
     if (lex)
         TWG_CUDA(c0, cudaMemsetAsync(c0->d_lex_tdone, 0, (size_t)B * c0->lex_tx * c0->lex_ty * sizeof(int), ms));
+    if (sh) {
+        // ghost rows beyond the global grid (top of slab 0, bottom of the last slab) are never
+        // exchanged and, with the shrinking launch ranges, never rewritten: keep them obstacle (+0.0,
+        // C4) in both ping-pong buffers, since an interval with an odd number of launches leaves
+        // the field in the other buffer
+        for (twg_ctx* c : g) {
+            const size_t bytes = (size_t)c->ghost * c->P * sizeof(float);
+            for (int q = 0; q < 2; ++q) {
+                if (c->shard.r0 == 0) TWG_CUDA(c, cudaMemsetAsync(c->u[q], 0, bytes, ms));
+                if (c->shard.r1 == c->shard.H_global)
+                    TWG_CUDA(c, cudaMemsetAsync(c->u[q] + (size_t)(c->H - c->ghost) * c->P, 0, bytes, ms));
+            }
+        }
+    }
 
     int lp = 0;  // launches so far (parity)
     if (maxs > 0) {

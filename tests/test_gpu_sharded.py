@@ -36,7 +36,9 @@ def _full(sc, S, check_every, tol, T=0):
     (3, 5, 101, 0, 0.0, 0),      # k < T: one 5-sweep launch per interval, remainder interval
     (4, 13, 77, 0, 0.0, 4),      # T = 4: launches 4, 4, 4, 1
     (2, 8, 3000, 8, 5e-4, 0),    # tolerance stop: the residual max is reduced across the slabs
-    (5, 3, 40, 0, 0.0, 2),       # thin slabs: no split (boundary bands would cover the interior)
+    (5, 3, 40, 0, 0.0, 2),       # launches 2 + 1 per interval
+    (10, 6, 61, 0, 0.0, 0),      # thin slabs (30 rows, G = 12): no split; one launch per interval, so
+                                 # the field alternates buffers between intervals
 ])
 def test_group_slabs_bit_identical(nslabs, k, S, check_every, tol, T):
     sc = scene_random("gslab", 300, 12, 25, 5)
