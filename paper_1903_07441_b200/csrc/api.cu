@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -67,6 +68,11 @@ static twg_status create_local(const twg_grid_desc* d, int32_t device, void* str
     c->d_res_bits = reinterpret_cast<unsigned*>(c->d_ctl + 4 * B);
     c->d_res = reinterpret_cast<float*>(c->d_ctl + 5 * B);
     c->d_flags = c->d_ctl + 6 * B;
+    CK(dev_alloc(&c->d_fixbox, 2 * B));
+    {
+        std::vector<int4> empty(2 * B, make_int4(1, 0, 1, 0));  // no positive fixed cell yet
+        CK(cudaMemcpy(c->d_fixbox, empty.data(), 2 * B * sizeof(int4), cudaMemcpyHostToDevice));
+    }
     CK(dev_alloc(&c->d_meta, B));
     CK(dev_alloc(&c->d_dir, cells));
     CK(cudaMemsetAsync(c->mask, 0, B * c->H * c->W, c->stream));
@@ -219,7 +225,7 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
         if (p != c) p->shard.peers.clear();
     void* ptrs[] = {c->u[0],     c->u[1],      c->mask,    c->d_ctl,   c->d_meta,   c->d_tracks,   c->d_t,
                     c->d_j,      c->d_pred,    c->d_boxes, c->d_param_block, c->d_track_off, c->d_cells, c->d_wp,
-                    c->d_smooth, c->d_track_tmp, c->d_dir, c->d_missed, c->d_trk_pred, c->d_trk_misn,
+                    c->d_smooth, c->d_track_tmp, c->d_dir, c->d_fixbox, c->d_missed, c->d_trk_pred, c->d_trk_misn,
                     c->d_trk_match, c->d_trk_used, c->d_trk_pairs, c->d_trk_ctl, c->d_trk_req, c->d_trk_det,
                     c->d_sim_rob, c->d_sim_int, c->d_sim_goal, c->d_sim_nobs, c->d_sim_obs, c->d_sim_obs_old,
                     c->d_sim_speed, c->d_sim_det, c->d_sim_hist, c->d_lex_tdone, c->d_lex_task, c->d_spec,
@@ -459,7 +465,11 @@ TWG_API twg_status twg_set_field(twg_ctx* c, int32_t b, const float* raw) {
         TWG_CUDA(c, cudaMemcpyAsync(tmp, raw, bytes, cudaMemcpyHostToDevice, c->stream));
         src = tmp;
     }
-    TWG_CUDA(c, launch_import(src, c->W, c->H, dst, c->P, c->stream));
+    int4* hb = nullptr;  // imported-field box: empty, then grown by k_import
+    TWG_CUDA(c, stage_alloc(c, sizeof(int4), reinterpret_cast<void**>(&hb)));
+    *hb = make_int4(std::numeric_limits<int>::max(), -1, std::numeric_limits<int>::max(), -1);
+    TWG_CUDA(c, cudaMemcpyAsync(c->d_fixbox + 2 * b + 1, hb, sizeof(int4), cudaMemcpyHostToDevice, c->stream));
+    TWG_CUDA(c, launch_import(src, c->W, c->H, dst, c->P, c->d_fixbox + 2 * b + 1, c->stream));
     c->launches += 1;
     if (tmp) TWG_CUDA(c, cudaFreeAsync(tmp, c->stream));
     TWG_CUDA(c, cudaStreamSynchronize(c->stream));

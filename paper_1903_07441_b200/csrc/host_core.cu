@@ -332,6 +332,7 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
     e.pred = c->d_pred;
     e.boxes = c->d_boxes;
     e.flags = c->d_flags;
+    e.fixbox = c->d_fixbox;
     e.cs = c->cs;
     e.ox = c->ox;
     e.oy = c->oy;
@@ -447,6 +448,11 @@ static twg_status launch_rb_range(twg_ctx* c, const twg_relax_cfg* cfg, int t, i
     a.res_r0 = c->ghost;
     a.res_r1 = c->H - c->ghost;
     a.lp = lp & 1;
+    a.fixbox = c->d_fixbox;
+    // TWG_RELAX_SLOW=1: every warp on the scalar path (tests); =2: no warp (timing experiments only --
+    // wrong results near positive fixed cells)
+    static const int force_slow = [] { const char* e = std::getenv("TWG_RELAX_SLOW"); return e ? std::atoi(e) : 0; }();
+    a.force_slow = force_slow;
     a.row_lo = lo;
     a.row_hi = hi;
     a.n_strips = (c->W + out_cols(t) - 1) / out_cols(t);

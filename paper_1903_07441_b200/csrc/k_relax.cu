@@ -97,6 +97,9 @@ struct Strip {
     unsigned rn;        // number of rows counted in the residual
     bool lane_out;
     float dmax;
+    // packed fast path near the goal (GOAL variant): the goal's absolute row, lane, column parity of its
+    // pair (0: a, 1: b) and element; ystart = absolute row of step 0
+    int ystart, gy, gl, gp, ge;
 };
 
 // Steps S, S+1, ..., NW-1 of one unrolled block of the row loop.  S is a template parameter so
@@ -107,6 +110,219 @@ __device__ __forceinline__ void block_steps(float4 (&win)[2 * T + 2], int ib, St
     win[S] = reinterpret_cast<const float4*>(st.rows + S * kStripW)[st.lane];
     wave_step<T, QOFF, RESID, S>(win, ib + S, st.hs, st.rlo, st.rn, st.lane_out, st.op, st.P, st.dmax);
     if constexpr (S + 1 < 2 * T + 2) block_steps<T, QOFF, RESID, S + 1>(win, ib, st);
+}
+
+// ---------------------------------------------------------------- packed fast path
+// Used by every warp whose region holds no positive fixed cell (the goal and any other fixed cell
+// with u > 0: RelaxArgs::fixbox); there the only fixed cells are obstacles, u = 0.  The four cells
+// of a lane are kept as two parity pairs -- a = columns (4l, 4l+2), b = (4l+1, 4l+3) -- so that the
+// two cells of one half-sweep are one register pair and the update runs on the sm_100a packed
+// FP32 pipe: (E+W), (N+S), their sum and the scaling are each ONE f32x2 instruction for both cells
+// (add.rn.f32x2 / mul.rn.f32x2: the same IEEE round-to-nearest operations as the scalar oracle, no
+// FTZ, so the result is bit-identical, C2).  No |.| is needed: in this region every value is <= 0
+// (free cells hold -u) or a zero (obstacle), so every sum is -(sum of the magnitudes) exactly
+// (round-to-nearest is sign-symmetric) and only the sign of a zero may differ.  The free/fixed
+// choice is a per-cell multiplier m (0.25 for a free cell, -0.0 for an obstacle, taken from the
+// sign bit when the row lands): u <- m ((E+W) + (N+S)) gives 0.25 (...) for a free cell and a zero
+// for an obstacle.  The stored encoding is restored when the row leaves: sign from m, magnitude
+// from the value (so a free cell whose value is a +0 is still stored as -0.0).
+struct FRow {
+    float2 a, b;    // values of the parity pairs
+    float2 ma, mb;  // their multipliers
+};
+
+__device__ __forceinline__ float2 f2add(float2 x, float2 y) {
+    float2 r;
+    asm("{\n.reg .b64 X, Y, R;\nmov.b64 X, {%2, %3};\nmov.b64 Y, {%4, %5};\nadd.rn.f32x2 R, X, Y;\n"
+        "mov.b64 {%0, %1}, R;\n}" : "=f"(r.x), "=f"(r.y) : "f"(x.x), "f"(x.y), "f"(y.x), "f"(y.y));
+    return r;
+}
+__device__ __forceinline__ float2 f2sub(float2 x, float2 y) {
+    float2 r;
+    asm("{\n.reg .b64 X, Y, R;\nmov.b64 X, {%2, %3};\nmov.b64 Y, {%4, %5};\nsub.rn.f32x2 R, X, Y;\n"
+        "mov.b64 {%0, %1}, R;\n}" : "=f"(r.x), "=f"(r.y) : "f"(x.x), "f"(x.y), "f"(y.x), "f"(y.y));
+    return r;
+}
+__device__ __forceinline__ float2 f2mul(float2 x, float2 y) {
+    float2 r;
+    asm("{\n.reg .b64 X, Y, R;\nmov.b64 X, {%2, %3};\nmov.b64 Y, {%4, %5};\nmul.rn.f32x2 R, X, Y;\n"
+        "mov.b64 {%0, %1}, R;\n}" : "=f"(r.x), "=f"(r.y) : "f"(x.x), "f"(x.y), "f"(y.x), "f"(y.y));
+    return r;
+}
+// 0.25 for a free cell (sign bit set), -0.0 for a fixed one.
+__device__ __forceinline__ float mult_of(float c) {
+    const int t = __float_as_int(c) >> 31;
+    return __int_as_float((t & 0x3E800000) | (~t & (int)0x80000000));
+}
+// Stored encoding of value v with multiplier m: |v| with the sign bit set iff the cell is free, i.e.
+// (v & 0x7fffffff) | (~m & 0x80000000) -- one LOP3 (LUT 0xB1 over v, m, 0x7fffffff).
+__device__ __forceinline__ float enc_of(float v, float m) {
+    float r;
+    asm("lop3.b32 %0, %1, %2, 0x7fffffff, 0xb1;" : "=f"(r) : "f"(v), "f"(m));
+    return r;
+}
+
+// The goal cell (u = 1, fixed) inside the fast path: held as -1 in registers like a free cell of u = 1
+// (its multiplier is the fixed one, so it is stored back as +1.0), and written back to -1 after every
+// half-sweep of its row and column parity.
+__device__ __forceinline__ void goal_patch(float2& nv, bool hit, int lane, const Strip& st) {
+    if (hit && lane == st.gl) {
+        if (st.ge) nv.y = -1.0f;
+        else nv.x = -1.0f;
+    }
+}
+
+template <int Q, bool TRACK, bool GOAL>
+__device__ __forceinline__ void hs_fast(FRow& c, const FRow& up, const FRow& dn, float& d, bool ghit, const Strip& st) {
+    // E + W of the two cells as two scalar FADDs (one operand is the neighbour lane's cell, so the
+    // pair would first have to be assembled), (N + S), the sum and the scaling packed
+    if (Q == 0) {  // cells 4l, 4l+2: E = (4l+1, 4l+3) = b, W = (4l-1, 4l+1)
+        const float l = __shfl_up_sync(0xffffffffu, c.b.y, 1);
+        const float2 ew = make_float2(c.b.x + l, c.b.y + c.b.x);
+        float2 nv = f2mul(f2add(ew, f2add(up.a, dn.a)), c.ma);
+        if (GOAL) goal_patch(nv, ghit, st.lane, st);
+        if (TRACK) {
+            const float2 dd = f2sub(nv, c.a);
+            d = fmaxf(fabsf(dd.x), fabsf(dd.y));
+        }
+        c.a = nv;
+    } else {  // cells 4l+1, 4l+3: E = (4l+2, 4l+4), W = (4l, 4l+2) = a
+        const float r = __shfl_down_sync(0xffffffffu, c.a.x, 1);
+        const float2 ew = make_float2(c.a.y + c.a.x, r + c.a.y);
+        float2 nv = f2mul(f2add(ew, f2add(up.b, dn.b)), c.mb);
+        if (GOAL) goal_patch(nv, ghit, st.lane, st);
+        if (TRACK) {
+            const float2 dd = f2sub(nv, c.b);
+            d = fmaxf(fabsf(dd.x), fabsf(dd.y));
+        }
+        c.b = nv;
+    }
+}
+
+// Half-sweep k of step S (row i - k of the strip, i = ib + S): the packed update plus, on the
+// residual sweeps, |du| of the owned rows.
+// `upr`: the row above (slot of row i - K - 1), passed separately because for K = 2T that slot may
+// already hold the next row (the interleaved order below loads row S + 1 early).
+// FIRST: the segment's first block, whose half-sweep k of step S only touches rows above every row
+// the stored rows depend on when 2k > S (those rows are never read by a needed update) -- skipped.
+template <int T, int QOFF, bool RESID, bool GOAL, bool FIRST, int S, int K>
+__device__ __forceinline__ void fast_hs(FRow (&win)[2 * T + 2], const FRow& upr, int i, const Strip& st,
+                                        float& dmax) {
+    if constexpr (FIRST && 2 * K > S) return;
+    constexpr int NW = 2 * T + 2;
+    constexpr int Qp = (S + 1 + QOFF) & 1;
+    constexpr int c = (S - K + 2 * NW) % NW, dn = (S - K + 1 + 2 * NW) % NW;
+    const bool ghit = GOAL && st.gp == Qp && st.ystart + i - K == st.gy;
+    if (RESID && K >= 2 * T - 1) {
+        float d = 0.0f;
+        hs_fast<Qp, true, GOAL>(win[c], upr, win[dn], d, ghit, st);
+        const int r = i - K - 2 * T;
+        if (st.lane_out && (unsigned)(r - st.rlo) < st.rn) dmax = fmaxf(dmax, d);
+    } else {
+        float d = 0.0f;
+        hs_fast<Qp, false, GOAL>(win[c], upr, win[dn], d, ghit, st);
+    }
+}
+template <int T, int S, int K>
+__device__ __forceinline__ const FRow& up_of(FRow (&win)[2 * T + 2]) {
+    return win[(S - K - 1 + 2 * (2 * T + 2)) % (2 * T + 2)];
+}
+
+template <int T, bool GOAL, int S>
+__device__ __forceinline__ void fast_load(FRow (&win)[2 * T + 2], const Strip& st) {
+    const float4 q = reinterpret_cast<const float4*>(st.rows + S * kStripW)[st.lane];
+    if (GOAL) {  // every value non-positive: the goal's +1.0 becomes -1 (obstacles -0, free cells unchanged)
+        const float4 n = make_float4(-fabsf(q.x), -fabsf(q.y), -fabsf(q.z), -fabsf(q.w));
+        win[S].a = make_float2(n.x, n.z);
+        win[S].b = make_float2(n.y, n.w);
+    } else {
+        win[S].a = make_float2(q.x, q.z);
+        win[S].b = make_float2(q.y, q.w);
+    }
+    win[S].ma = make_float2(mult_of(q.x), mult_of(q.z));
+    win[S].mb = make_float2(mult_of(q.y), mult_of(q.w));
+}
+
+// Row i - 2T is final after step S: store it (stored encoding, predicated store -- no divergent branch,
+// so the following shuffles need no reconvergence).
+template <int T, int S>
+__device__ __forceinline__ void fast_store(FRow (&win)[2 * T + 2], int i, Strip& st) {
+    constexpr int NW = 2 * T + 2;
+    constexpr int so = (S - 2 * T + 2 * NW) % NW;
+    const FRow& w = win[so];
+    const float4 o =
+        make_float4(enc_of(w.a.x, w.ma.x), enc_of(w.b.x, w.mb.x), enc_of(w.a.y, w.ma.y), enc_of(w.b.y, w.mb.y));
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\n@p st.global.v4.f32 [%0], {%1, %2, %3, %4};\n}" ::"l"(st.op),
+                 "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w), "r"((st.lane_out && (unsigned)(i - 4 * T) < st.hs) ? 1 : 0));
+    st.op += st.P;
+}
+
+// Steps S and S + 1 with their half-sweeps interleaved along the anti-diagonals of the wavefront:
+// (S, k) needs (S, k - 1), (S - 1, k - 1) and (S - 2, k - 1) only, so (S, k) and (S + 1, k - 1) are
+// independent and issue back to back -- two dependency chains per warp instead of one.
+template <int T, int QOFF, bool RESID, bool GOAL, bool FIRST, int S, int K>
+__device__ __forceinline__ void fast_pair_hs(FRow (&win)[2 * T + 2], const FRow& last_up, int ib, const Strip& st,
+                                             float& dmax) {
+    if constexpr (K <= 2 * T) {
+        if constexpr (K == 2 * T) fast_hs<T, QOFF, RESID, GOAL, FIRST, S, K>(win, last_up, ib + S, st, dmax);
+        else fast_hs<T, QOFF, RESID, GOAL, FIRST, S, K>(win, up_of<T, S, K>(win), ib + S, st, dmax);
+        fast_hs<T, QOFF, RESID, GOAL, FIRST, S + 1, K - 1>(win, up_of<T, S + 1, K - 1>(win), ib + S + 1, st, dmax);
+        fast_pair_hs<T, QOFF, RESID, GOAL, FIRST, S, K + 1>(win, last_up, ib, st, dmax);
+    }
+}
+
+template <int T, int QOFF, bool RESID, bool GOAL, bool FIRST, int S>
+__device__ __forceinline__ void block_steps_fast(FRow (&win)[2 * T + 2], int ib, Strip& st) {
+    constexpr int NW = 2 * T + 2;
+    float dmax = st.dmax;
+    fast_load<T, GOAL, S>(win, st);
+    fast_hs<T, QOFF, RESID, GOAL, FIRST, S, 1>(win, up_of<T, S, 1>(win), ib + S, st, dmax);
+    // row S + 1 lands in the slot of row S - 2T - 1, which (S, 2T) still reads as its upper neighbour
+    const FRow last_up = win[(S + 1) % NW];
+    fast_load<T, GOAL, S + 1>(win, st);
+    fast_pair_hs<T, QOFF, RESID, GOAL, FIRST, S, 2>(win, last_up, ib, st, dmax);
+    fast_store<T, S>(win, ib + S, st);
+    fast_hs<T, QOFF, RESID, GOAL, FIRST, S + 1, 2 * T>(win, up_of<T, S + 1, 2 * T>(win), ib + S + 1, st, dmax);
+    fast_store<T, S + 1>(win, ib + S + 1, st);
+    st.dmax = dmax;
+    if constexpr (S + 2 < 2 * T + 2) block_steps_fast<T, QOFF, RESID, GOAL, FIRST, S + 2>(win, ib, st);
+}
+
+// The fast path's row loop.  has_goal: the goal cell lies in the warp's region; it is loaded at step
+// i0 = gy - ystart, updated at steps i0 + 1 .. i0 + 2T and read by its neighbours until step
+// i0 + 2T + 1, so only the (at most two) blocks holding steps i0 .. i0 + 2T run the GOAL variant (load
+// as -|u|, write the goal back after its half-sweeps); outside them the goal row is either not yet
+// loaded or only read (its -1 is kept in the register).
+template <int T, int QOFF, bool RESID>
+__device__ __forceinline__ void fast_rows(float* ring, uint64_t* bars, const CUtensorMap* tmap, int xb, int b, int nblk,
+                                          bool has_goal, Strip& st) {
+    constexpr int NW = 2 * T + 2;
+    constexpr int STAGE_F = NW * kStripW;
+    FRow win[NW];
+#pragma unroll
+    for (int s = 0; s < NW; ++s) win[s] = FRow{make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                               make_float2(0.f, 0.f)};
+    const int i0 = st.gy - st.ystart;
+    for (int blk = 0; blk < nblk; ++blk) {
+        const int sg = blk % kStages;
+        mbar_wait(&bars[sg], (blk / kStages) & 1);
+        st.rows = ring + sg * STAGE_F;
+        const bool gblk = has_goal && blk * NW <= i0 + 2 * T && blk * NW + NW - 1 >= i0;
+        if (blk == 0) {
+            if (gblk) block_steps_fast<T, QOFF, RESID, true, true, 0>(win, 0, st);
+            else block_steps_fast<T, QOFF, RESID, false, true, 0>(win, 0, st);
+        } else {
+            if (gblk) block_steps_fast<T, QOFF, RESID, true, false, 0>(win, blk * NW, st);
+            else block_steps_fast<T, QOFF, RESID, false, false, 0>(win, blk * NW, st);
+        }
+        if (blk + kStages < nblk) {
+            __syncwarp();
+            if (st.lane == 0) {
+                mbar_expect_tx(&bars[sg], STAGE_F * 4);
+                tma_load_3d(ring + sg * STAGE_F, tmap, xb, st.ystart + (blk + kStages) * NW, b, &bars[sg]);
+            }
+        }
+    }
 }
 
 template <int T, int QOFF, bool RESID>
@@ -159,22 +375,44 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     // row i - 4T of the segment is finalised at step i: start 4T rows above the first output row
     st.op = (src ? a.u0 : a.u1) + (int64_t)b * a.sstride + (int64_t)(y0 - 4 * T) * a.P + x;
     st.dmax = 0.0f;
-    float4 win[NW];
+    // the packed fast path unless the warp's region [xb, xb + 128) x [ystart, ystart + nblk NW) holds a
+    // positive fixed cell (goal box, imported-field box) -- warp-uniform
+    // the goal (box 0, a single cell) takes the fast path's GOAL variant; any other positive fixed cell
+    // (box 1: an imported field) the scalar path
+    bool slow = a.force_slow == 1, goal = false;
+    st.ystart = ystart;
+    if (a.fixbox != nullptr && a.force_slow != 2) {
+        const int yend = ystart + nblk * NW - 1;
+        auto hits = [&](const int4 fb) {  // (x0, x1, y0, y1), empty when x0 > x1
+            return fb.x <= fb.y && fb.x <= xb + kStripW - 1 && fb.y >= xb && fb.z <= yend && fb.w >= ystart;
+        };
+        const int4 g = a.fixbox[2 * b];
+        slow = slow || hits(a.fixbox[2 * b + 1]) || (hits(g) && (g.x != g.y || g.z != g.w));
+        goal = !slow && hits(g);
+        st.gy = g.z;
+        st.gl = (g.x - xb) >> 2;
+        st.gp = (g.x - xb) & 1;
+        st.ge = ((g.x - xb) >> 1) & 1;
+    }
+    if (slow) {
+        float4 win[NW];
 #pragma unroll
-    for (int s = 0; s < NW; ++s) win[s] = make_float4(0.f, 0.f, 0.f, 0.f);
-
-    for (int blk = 0; blk < nblk; ++blk) {
-        const int sg = blk % kStages;
-        mbar_wait(&bars[sg], (blk / kStages) & 1);
-        st.rows = ring + sg * STAGE_F;
-        block_steps<T, QOFF, RESID, 0>(win, blk * NW, st);
-        if (blk + kStages < nblk) {
-            __syncwarp();  // every lane has consumed stage sg (its values are in registers)
-            if (lane == 0) {
-                mbar_expect_tx(&bars[sg], STAGE_F * 4);
-                tma_load_3d(ring + sg * STAGE_F, tmap, xb, ystart + (blk + kStages) * NW, b, &bars[sg]);
+        for (int s = 0; s < NW; ++s) win[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int blk = 0; blk < nblk; ++blk) {
+            const int sg = blk % kStages;
+            mbar_wait(&bars[sg], (blk / kStages) & 1);
+            st.rows = ring + sg * STAGE_F;
+            block_steps<T, QOFF, RESID, 0>(win, blk * NW, st);
+            if (blk + kStages < nblk) {
+                __syncwarp();  // every lane has consumed stage sg (its values are in registers)
+                if (lane == 0) {
+                    mbar_expect_tx(&bars[sg], STAGE_F * 4);
+                    tma_load_3d(ring + sg * STAGE_F, tmap, xb, ystart + (blk + kStages) * NW, b, &bars[sg]);
+                }
             }
         }
+    } else {
+        fast_rows<T, QOFF, RESID>(ring, bars, tmap, xb, b, nblk, goal, st);
     }
 
     pdl_trigger();

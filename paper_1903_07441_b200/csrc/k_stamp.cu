@@ -27,6 +27,7 @@ __global__ void k_encode_cold(EncodeArgs e) {
     const int b = sp.b;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x == 0 && y == 0) e.fixbox[2 * b + 1] = make_int4(1, 0, 1, 0);  // no imported fixed values left
     if (y >= e.H || x >= e.P) return;
     float v = 0.0f;  // pad columns: fixed obstacle
     if (x < e.W) v = e.mask[((int64_t)b * e.H + y) * e.W + x] ? 0.0f : -0.5f;
@@ -60,7 +61,11 @@ __device__ __forceinline__ void goal_reset_one(const EncodeArgs& e, const ScenPa
 }
 
 __device__ __forceinline__ void set_goal_one(const EncodeArgs& e, const ScenParams& sp) {
-    if (sp.gy < 0 || sp.gy >= e.H) return;  // the goal lies in another row slab
+    const bool in = sp.gy >= 0 && sp.gy < e.H;  // else the goal lies in another row slab
+    // the goal is the field's positive fixed cell: its box keeps k_rb_tblock's nearby warps on the
+    // scalar path
+    e.fixbox[2 * sp.b] = in ? make_int4(sp.gx, sp.gx, sp.gy, sp.gy) : make_int4(1, 0, 1, 0);
+    if (!in) return;
     (sp.cur ? e.u1 : e.u0)[(int64_t)sp.b * e.sstride + (int64_t)sp.gy * e.P + sp.gx] = 1.0f;
 }
 
@@ -248,12 +253,23 @@ __global__ void k_convert(const float* __restrict__ src, int64_t P, int W, int H
     dst[(int64_t)y * W + x] = mode == 0 ? v : (mode == 1 ? fabsf(v) : 1.0f - fabsf(v));
 }
 
-// Field import (twg_set_field): dense raw -> pitched, pad columns +0.0.
-__global__ void k_import(const float* __restrict__ src, int W, int H, float* __restrict__ dst, int64_t P) {
+// Field import (twg_set_field): dense raw -> pitched, pad columns +0.0; the bounding box of the
+// positive cells (fixed cells with u > 0, e.g. the goal or Dirichlet test data) is accumulated into
+// box (x0, x1, y0, y1), which the caller set empty.
+__global__ void k_import(const float* __restrict__ src, int W, int H, float* __restrict__ dst, int64_t P,
+                         int4* __restrict__ box) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= P || y >= H) return;
-    dst[(int64_t)y * P + x] = x < W ? src[(int64_t)y * W + x] : 0.0f;
+    const float v = x < W ? src[(int64_t)y * W + x] : 0.0f;
+    dst[(int64_t)y * P + x] = v;
+    if (__float_as_int(v) > 0) {
+        int* b = reinterpret_cast<int*>(box);
+        atomicMin(b + 0, x);
+        atomicMax(b + 1, x);
+        atomicMin(b + 2, y);
+        atomicMax(b + 3, y);
+    }
 }
 
 cudaError_t launch_convert(const float* src, int64_t P, int W, int H, float* dst, int mode, cudaStream_t st) {
@@ -263,10 +279,10 @@ cudaError_t launch_convert(const float* src, int64_t P, int W, int H, float* dst
     return cudaGetLastError();
 }
 
-cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P, cudaStream_t st) {
+cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P, int4* box, cudaStream_t st) {
     dim3 blk(128, 4);
     dim3 grid((unsigned)((P + 127) / 128), (H + 3) / 4);
-    k_import<<<grid, blk, 0, st>>>(src, W, H, dst, P);
+    k_import<<<grid, blk, 0, st>>>(src, W, H, dst, P, box);
     return cudaGetLastError();
 }
 

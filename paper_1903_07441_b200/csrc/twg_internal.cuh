@@ -45,6 +45,8 @@ struct RelaxArgs {
     int res_r0, res_r1;  // rows whose cells count in the residual (owned rows of a slab)
     const int* done;     // per-scenario done flags
     unsigned* res;       // per-scenario residual (float bits, atomicMax), used when RESID
+    const int4* fixbox;  // [B][2] boxes (x0, x1, y0, y1) of the positive fixed cells: goal, imported field
+    int force_slow;      // 1: every warp takes the scalar path (TWG_RELAX_SLOW=1, tests)
 };
 
 // Per-scenario parameters of one encode (rows a1-a3), built on the host.
@@ -206,6 +208,7 @@ struct twg_ctx {
     float* d_res = nullptr;
     int* d_where = nullptr;
     int* d_flags = nullptr;
+    int4* d_fixbox = nullptr;      // [B][2]: goal box, imported-field box (k_rb_tblock's fast path)
     // encode state
     struct Scen {
         int gx = -1, gy = -1, rcx = -1, rcy = -1;

@@ -50,7 +50,7 @@ cudaError_t launch_check(int B, int* done, int* sweeps, unsigned* res_bits, floa
                          int check_every, int max_sweeps, float tol, const int* cur, int lp, cudaStream_t st);
 cudaError_t launch_init_field(float* u, int64_t P, int64_t sstride, int W, int H, int B, cudaStream_t st);
 cudaError_t launch_convert(const float* src, int64_t P, int W, int H, float* dst, int mode, cudaStream_t st);
-cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P, cudaStream_t st);
+cudaError_t launch_import(const float* src, int W, int H, float* dst, int64_t P, int4* box, cudaStream_t st);
 cudaError_t launch_fixup(float* u0, float* u1, int64_t sstride, int B, const int* where, const int* cur, int lp,
                          cudaStream_t st);
 
@@ -73,6 +73,7 @@ struct EncodeArgs {
     double* pred;          // [B][cap][3]
     int4* boxes;           // [B][cap]
     int* flags;            // [B] warning flags
+    int4* fixbox;          // [B][2]: goal box (set with the goal), imported-field box (cleared by a cold encode)
     double cs, ox, oy;
 };
 cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_tracks, int any_cold, int* n_launch,
