@@ -430,6 +430,25 @@ TWG_API twg_status twg_walk_from(twg_ctx* ctx, int32_t b, int32_t x, int32_t y, 
  * ghost rows use the local grid only.  Errors: INVALID_ARG, CUDA. */
 TWG_API twg_status twg_index_matrix(twg_ctx* ctx, int32_t b, uint8_t* out);
 
+/* Per-cell rubber band on the index matrix (Alg. 1 P:701-704 "for each cell
+ * in the index matrix in parallel: calculate tension force T and potential
+ * force F via Eq. 6; update the index matrix with the position of the
+ * neighbor with the minimum resultant force (Eqs. 4-5)", then P:705
+ * "generate the current path based on the optimized index matrix"; SURVEY
+ * 8(f) f3; reading C37): M_idx of Eq. 3 for scenario b's current field, then
+ * cfg->iterations iterations (cells with (x + y) even, then odd) in which
+ * every free cell c picks, among its in-grid non-obstacle 4-neighbours n with
+ * u > 1e-9, the successor minimising |R|^2, R = -F d + k_t (c - n) +
+ * k_t (M(n) - n), F = 1/u(n) - 1/u(c) (C13), the current successor kept on
+ * ties, the others in the order +x, -x, +y, -y; then the walk along the
+ * optimised matrix from the robot cell.  out[height x width] (host or device,
+ * may be NULL): the optimised matrix (codes of twg_index_matrix); cells_xy
+ * (host, max_len (x, y) pairs, may be NULL), *n_cells: the walk.  Not on row
+ * slabs.  Returns OK or NO_PATH (the walk met an obstacle, a successor-less
+ * cell or exceeded max_len; *n_cells = 0); INVALID_ARG, CUDA. */
+TWG_API twg_status twg_band_index(twg_ctx* ctx, int32_t b, const twg_band_cfg* cfg, uint8_t* out, int32_t* cells_xy,
+                                  int32_t* n_cells);
+
 /* Per-cell warp number (the paper's kernel 1, "calculate the warp
  * of each cell"; the numbered ellipses of P:438-456):
  * out[height x width] int32 row-major (host or device), t = max(1,

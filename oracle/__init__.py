@@ -89,6 +89,10 @@ def lib():
         L.orc_sim_move.restype = None
         L.orc_sim_move.argtypes = [i32, i32, d, d, d, P, P, P, P, d, d, i32, d, d, i32, P, P, P, i32, u64, u64,
                                    P, P]
+        L.orc_cellband.restype = None
+        L.orc_cellband.argtypes = [i32, i32, P, P, P, i32, f32]
+        L.orc_walk_dir.restype = i32
+        L.orc_walk_dir.argtypes = [i32, i32, P, i32, i32, i32, P, P]
         L.orc_warp_map.restype = None
         L.orc_warp_map.argtypes = [i32, i32, d, d, d, d, d, d, d, P]
         L.orc_init_u32.restype = None
@@ -280,6 +284,27 @@ def index_matrix(cls, u):
     H, W = u.shape
     lib().orc_index_matrix(W, H, _p(cls), _p(u), _p(out))
     return out
+
+
+def cellband(cls, u, dir_in, iters=50, kt=1.0):
+    """Per-cell rubber band on the index matrix (orc_cellband, Alg. 1, C37): returns the
+    optimised matrix (dir_in is not modified)."""
+    cls = np.ascontiguousarray(cls, np.uint8)
+    u = np.ascontiguousarray(u, np.float32)
+    d = np.ascontiguousarray(dir_in, np.uint8).copy()
+    H, W = u.shape
+    lib().orc_cellband(W, H, _p(cls), _p(u), _p(d), int(iters), np.float32(kt))
+    return d
+
+
+def walk_dir(dir_m, start, max_len):
+    """Walk along an index matrix from start (orc_walk_dir): (status, cells [n, 2])."""
+    d = np.ascontiguousarray(dir_m, np.uint8)
+    H, W = d.shape
+    cells = np.zeros((max(max_len, 1), 2), np.int32)
+    n = np.zeros(1, np.int32)
+    st = lib().orc_walk_dir(W, H, _p(d), int(start[0]), int(start[1]), int(max_len), _p(cells), _p(n))
+    return st, cells[: int(n[0])].copy()
 
 
 def warp_map(scene):

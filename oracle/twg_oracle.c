@@ -513,6 +513,82 @@ void orc_index_matrix(int32_t W, int32_t H, const uint8_t* cls, const float* u, 
         }
 }
 
+/* Per-cell rubber band on the index matrix (Alg. 1 P:701-704 "for each cell in the index matrix in
+ * parallel: calculate tension force T and potential force F via Eq. 6; update the index matrix with
+ * the position of the neighbor with the minimum resultant force (Eqs. 4-5)"; reading
+ * C37 of DESIGN.md).  A cell has one successor but possibly several predecessors, so the band acts on
+ * the successor: for a free cell c with current successor m = M(c), each candidate n among its
+ * in-grid, non-obstacle 4-neighbours is scored by the resultant force on n were the link c -> n ->
+ * M(n):
+ *   R(n) = F_vec + k_t (c - n) + k_t (M(n) - n),  F = 1/u(n) - 1/u(c),  F_vec = -F d (d = n - c,
+ *   a unit axis vector; Eq. 6 in u-space as C13), where M(n) is the cell n's successor (n itself
+ *   when n is the goal, an obstacle or has none: no tension from it);
+ * candidates with u(n) <= 1e-9 or u(c) <= 1e-9 are skipped (C13).  The current successor is scored
+ * first and kept on ties; the others follow in the order +x, -x, +y, -y with strict < (C8).  One
+ * iteration updates the cells with (x + y) even, then those with (x + y) odd: a cell reads only its
+ * neighbours' successors, which have the other colour, so each phase is order-free.  dir: H x W in/out,
+ * codes of orc_index_matrix (0..3 = +x, -x, +y, -y; 4 goal, 5 obstacle, 6 none); goal, obstacle
+ * and successor-less cells are not changed.  Parity pinned by hand (P27). */
+void orc_cellband(int32_t W, int32_t H, const uint8_t* cls, const float* u, uint8_t* dir, int32_t iters, float kt)
+{
+    static const int dxs[4] = { +1, -1, 0, 0 };
+    static const int dys[4] = { 0, 0, +1, -1 };
+    for (int32_t it = 0; it < iters; ++it)
+        for (int color = 0; color < 2; ++color)
+            for (int32_t y = 0; y < H; ++y)
+                for (int32_t x = 0; x < W; ++x) {
+                    if (((x + y) & 1) != color) continue;
+                    size_t q = (size_t)y * W + x;
+                    if (cls[q] != ORC_FREE || dir[q] > 3) continue;
+                    float uc = u[q];
+                    if (uc <= 1e-9f) continue;
+                    int best_d = dir[q];
+                    float best = 0.0f;
+                    int have = 0;
+                    for (int pass = 0; pass < 5; ++pass) {
+                        int d = pass == 0 ? dir[q] : pass - 1;
+                        if (pass > 0 && d == dir[q]) continue;
+                        int nx = x + dxs[d], ny = y + dys[d];
+                        if (nx < 0 || ny < 0 || nx >= W || ny >= H) continue;
+                        size_t qn = (size_t)ny * W + nx;
+                        if (cls[qn] == ORC_OBSTACLE) continue;
+                        float un = u[qn];
+                        if (un <= 1e-9f) continue;
+                        int mx = nx, my = ny;  /* n's successor */
+                        if (dir[qn] <= 3) { mx = nx + dxs[dir[qn]]; my = ny + dys[dir[qn]]; }
+                        float F = 1.0f / un - 1.0f / uc;
+                        float Rx = (-(F * (float)dxs[d]) + kt * (float)(x - nx)) + kt * (float)(mx - nx);
+                        float Ry = (-(F * (float)dys[d]) + kt * (float)(y - ny)) + kt * (float)(my - ny);
+                        float r2 = Rx * Rx + Ry * Ry;
+                        if (!have || r2 < best) { best = r2; best_d = d; have = 1; }
+                    }
+                    dir[q] = (uint8_t)best_d;
+                }
+}
+
+/* Walk along an index matrix (codes of orc_index_matrix) from (sx, sy): the cells visited, the start
+ * included, until the goal (ORC_OK); an obstacle, a successor-less cell or more than max_len cells
+ * is ORC_E_NO_PATH (*n_cells = 0).  Used to generate the path from the per-cell band's matrix
+ * (Alg. 1 P:705 "Generate the current path based on the optimized index matrix"). */
+int32_t orc_walk_dir(int32_t W, int32_t H, const uint8_t* dir, int32_t sx, int32_t sy, int32_t max_len,
+                     int32_t* cells_xy, int32_t* n_cells)
+{
+    static const int dxs[4] = { +1, -1, 0, 0 };
+    static const int dys[4] = { 0, 0, +1, -1 };
+    int32_t n = 0, x = sx, y = sy;
+    *n_cells = 0;
+    if (max_len < 1) return ORC_E_NO_PATH;
+    cells_xy[0] = x; cells_xy[1] = y; n = 1;
+    for (;;) {
+        uint8_t d = dir[(size_t)y * W + x];
+        if (d == 4) { *n_cells = n; return ORC_OK; }
+        if (d > 3) return ORC_E_NO_PATH;
+        if (n + 1 > max_len) return ORC_E_NO_PATH;
+        x += dxs[d]; y += dys[d];
+        cells_xy[2 * n] = x; cells_xy[2 * n + 1] = y; ++n;
+    }
+}
+
 /* Per-cell warp number (the paper's kernel 1, "calculate the warp of each cell"; the
  * numbered ellipses of Fig. warps): t of an obstacle at the cell centre. */
 void orc_warp_map(int32_t W, int32_t H, double cs, double ox, double oy, double xr, double yr, double theta,

@@ -38,11 +38,9 @@ TWG_API twg_status twg_walk_from(twg_ctx* c, int32_t b, int32_t x, int32_t y, in
     return TWG_OK;
 }
 
-TWG_API twg_status twg_index_matrix(twg_ctx* c, int32_t b, uint8_t* out) {
-    twg_status st = check_ctx(c);
-    if (st != TWG_OK) return st;
-    if (!out || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
-    st = ensure_params(c, 1);
+// Shared by twg_index_matrix and twg_band_index: Eq. 3 for every cell of scenario b into d_dir.
+static twg_status index_matrix_core(twg_ctx* c, int32_t b) {
+    twg_status st = ensure_params(c, 1);
     if (st != TWG_OK) return st;
     ScenParams sp;
     std::memset(&sp, 0, sizeof(sp));
@@ -66,6 +64,49 @@ TWG_API twg_status twg_index_matrix(twg_ctx* c, int32_t b, uint8_t* out) {
     p.istride = c->sstride;
     TWG_CUDA(c, launch_index_dir(p, c->stream));
     c->launches += 1;
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_band_index(twg_ctx* c, int32_t b, const twg_band_cfg* cfg, uint8_t* out, int32_t* cells_xy,
+                                  int32_t* n_cells) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!cfg || b < 0 || b >= c->B || cfg->iterations < 0 || cfg->max_len < 1)
+        return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    if (c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "the per-cell band is not available on a row slab");
+    const twg_ctx::Scen& sc = c->scen[b];
+    if (!sc.encoded) return fail(c, TWG_E_INVALID_ARG, "twg_band_index before set_obstacles");
+    st = index_matrix_core(c, b);
+    if (st != TWG_OK) return st;
+    uint8_t* dir = c->d_dir + (int64_t)b * c->sstride;
+    const float* f = c->u[c->cur[b]] + (int64_t)b * c->sstride;
+    int nl = 0;
+    TWG_CUDA(c, launch_cellband(f, c->P, c->W, c->H, dir, cfg->iterations, cfg->k_t, &nl, c->stream));
+    c->launches += nl;
+    if (out)
+        TWG_CUDA(c, cudaMemcpy2DAsync(out, c->W, dir, c->P, c->W, c->H, cudaMemcpyDefault, c->stream));
+    int* d = nullptr;
+    TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&d), (2 + 2 * (size_t)cfg->max_len) * sizeof(int), c->stream));
+    TWG_CUDA(c, launch_walk_dir(dir, c->P, sc.rcx, sc.rcy, cfg->max_len, d, reinterpret_cast<int2*>(d + 2), c->stream));
+    c->launches += 1;
+    int h[2];
+    TWG_CUDA(c, cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (cells_xy && h[1] > 0)
+        TWG_CUDA(c, cudaMemcpy(cells_xy, d + 2, (size_t)h[1] * 2 * sizeof(int), cudaMemcpyDeviceToHost));
+    TWG_CUDA(c, cudaFreeAsync(d, c->stream));
+    TWG_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (n_cells) *n_cells = h[1];
+    if (h[0] != TWG_OK) return fail(c, TWG_E_NO_PATH, "no path along the optimised index matrix");
+    return TWG_OK;
+}
+
+TWG_API twg_status twg_index_matrix(twg_ctx* c, int32_t b, uint8_t* out) {
+    twg_status st = check_ctx(c);
+    if (st != TWG_OK) return st;
+    if (!out || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
+    st = index_matrix_core(c, b);
+    if (st != TWG_OK) return st;
     // [H][P] -> [H][W] (cudaMemcpyDefault: out may be host or device)
     TWG_CUDA(c, cudaMemcpy2DAsync(out, c->W, c->d_dir + (int64_t)b * c->sstride, c->P, c->W, c->H, cudaMemcpyDefault,
                                   c->stream));

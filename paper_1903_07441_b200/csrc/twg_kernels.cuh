@@ -126,6 +126,11 @@ struct PathArgs {
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
 cudaError_t launch_index_dir(const PathArgs& p, cudaStream_t st);  // k_index_dir alone (twg_index_matrix)
+// f3 per-cell band on the index matrix (2 iters launches) and the walk along a matrix
+cudaError_t launch_cellband(const float* f, int64_t P, int W, int H, uint8_t* dir, int iters, float kt, int* n_launch,
+                            cudaStream_t st);
+cudaError_t launch_walk_dir(const uint8_t* dir, int64_t P, int x, int y, int max_len, int* out, int2* cells,
+                            cudaStream_t st);
 cudaError_t launch_walk_from(const float* f, int64_t P, int W, int H, int r0, int r1, int x, int y, int max_cells,
                              int* cells, int* out, cudaStream_t st);
 

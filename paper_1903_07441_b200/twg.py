@@ -107,6 +107,7 @@ SIGNATURES = [
     ("twg_walk_from", C.c_int32, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32), _P]),
     ("twg_index_matrix", C.c_int32, [_P, C.c_int32, _P]),
+    ("twg_band_index", C.c_int32, [_P, C.c_int32, C.POINTER(BandCfg), _P, _P, C.POINTER(C.c_int32)]),
     ("twg_warp_map", C.c_int32, [_P, C.POINTER(Robot), C.c_double, _P]),
     ("twg_field_ptr", C.c_int32, [_P, C.c_int32, C.POINTER(_P), C.POINTER(C.c_int64)]),
     ("twg_debug_walk", C.c_int32, [_P, C.c_int32, _P]),
@@ -407,6 +408,15 @@ class Planner:
         out = np.zeros((self.H, self.W), np.uint8) if out is None else out
         _check(self.ctx, lib().twg_index_matrix(self.ctx, b, _ptr(out)))
         return out
+
+    def band_index(self, b, cfg, out=None):
+        """twg_band_index (f3 per-cell band): (status, optimised uint8 [H, W] matrix, walk cells [n, 2])."""
+        out = np.zeros((self.H, self.W), np.uint8) if out is None else out
+        cells = np.zeros((cfg.max_len, 2), np.int32)
+        n = C.c_int32()
+        st = lib().twg_band_index(self.ctx, b, C.byref(cfg), _ptr(out), _ptr(cells), C.byref(n))
+        _check(self.ctx, st, ok=(OK, E_NO_PATH))
+        return st, out, cells[: n.value].copy()
 
     def warp_map(self, robot, warp_spacing=1.0, out=None):
         """twg_warp_map: int32 [H, W] warp number of every cell centre for the robot pose."""

@@ -299,3 +299,77 @@ def test_p26_warm_init_by_hand(orc):
     assert orc.init_u32(cls_prev, prev, cls_prev).tolist() == [[0.375, 0.0, 1.0], [0.75, 0.25, 0.125]]
     # cold: free 0.5
     assert orc.init_u32(cls).tolist() == [[0.5, 0.5, 0.5], [0.0, 1.0, 0.5]]
+
+
+# --------------------------------------------------------------------- P27 (f3 per-cell band, C37)
+def test_p27_cellband_2x2_by_hand(orc):
+    # goal (1,1); u(1,0) = 0.5, u(0,1) = 0.4, u(0,0) = 0.25.  Eq. 3: M(0,0) = +x (0.5 > 0.4).
+    # Per-cell band (Alg. 1, reading C37), k_t = 1, cell (0,0):
+    #   n = (1,0): F = 1/0.5 - 1/0.25 = -2, M(n) = goal -> R = (-F - 1, 1) = (1, 1), |R|^2 = 2
+    #   n = (0,1): F = 1/0.4 - 1/0.25 = -1.5, M(n) = goal -> R = (1, -F - 1) = (1, 0.5), |R|^2 = 1.25
+    # so (0,0) switches to +y (code 2); (1,0) and (0,1) point at the goal with R = 0 and keep it.
+    cls = np.array([[0, 0], [0, orc.GOAL]], np.uint8)
+    u = np.array([[0.25, 0.5], [0.4, 1.0]], np.float32)
+    m = orc.index_matrix(cls, u)
+    assert m.tolist() == [[0, 2], [0, 4]]
+    b = orc.cellband(cls, u, m, iters=1)
+    assert b.tolist() == [[2, 2], [0, 4]]
+    st, cells = orc.walk_dir(b, (0, 0), 10)
+    assert st == orc.OK and cells.tolist() == [[0, 0], [0, 1], [1, 1]]
+    # more iterations change nothing (a fixed point), I = 0 is the identity
+    assert np.array_equal(orc.cellband(cls, u, m, iters=5), b)
+    assert np.array_equal(orc.cellband(cls, u, m, iters=0), m)
+
+
+def test_p27_cellband_3x3_centre_goal_is_a_fixed_point(orc):
+    # the exact fixed point of P5 (edges u = 1/3, corners 1/6): an edge keeps the goal (|R|^2 = (3 - 2)^2
+    # = 1 against (6 - 3 + 2)^2 = 25 for a corner), a corner's two candidates tie (both |R|^2 =
+    # (F + 1)^2 + 1) and the current successor is kept
+    cls = np.zeros((3, 3), np.uint8)
+    cls[1, 1] = orc.GOAL
+    u = orc.init_u32(cls)
+    orc.relax_f32(cls, u, 1000, 1, 0.0)
+    m = orc.index_matrix(cls, u)
+    assert np.array_equal(orc.cellband(cls, u, m, iters=10), m)
+
+
+def test_p27_cellband_straight_corridor_unchanged(orc):
+    # a 1-wide corridor: every cell's only alternatives are walls or the cell behind it, whose
+    # tensions point forward (2 k_t) -- the matrix stays the steepest-ascent one
+    W = 12
+    cls = np.ones((3, W), np.uint8)
+    cls[1, :] = 0
+    cls[1, W - 1] = orc.GOAL
+    u = orc.init_u32(cls)
+    orc.relax_f32(cls, u, 10000, 1, 0.0)
+    m = orc.index_matrix(cls, u)
+    assert (m[1, :W - 1] == 0).all()
+    assert np.array_equal(orc.cellband(cls, u, m, iters=50), m)
+
+
+def test_p27_cellband_properties_random_maps(orc):
+    # on random converged maps: goal / obstacle / successor-less codes never change, every code the band
+    # changed points at an in-grid non-obstacle neighbour (Eq. 3's own choice may be an obstacle in a
+    # goal-less region, u = 0, which the band skips); the walk along Eq. 3's matrix is the implicit walk
+    rng = np.random.default_rng(27)
+    for trial in range(20):
+        H, W = int(rng.integers(5, 30)), int(rng.integers(5, 30))
+        cls = (rng.random((H, W)) < 0.15).astype(np.uint8)
+        gy, gx = int(rng.integers(0, H)), int(rng.integers(0, W))
+        cls[gy, gx] = orc.GOAL
+        u = orc.init_u32(cls)
+        orc.relax_f32(cls, u, 3000, 1, 0.0)
+        m = orc.index_matrix(cls, u)
+        b = orc.cellband(cls, u, m, iters=int(rng.integers(1, 20)), kt=float(rng.choice([0.5, 1.0, 2.0])))
+        assert np.array_equal(b[m > 3], m[m > 3])
+        ys, xs = np.nonzero((b <= 3) & (b != m))
+        dx = np.array([1, -1, 0, 0])[b[ys, xs]]
+        dy = np.array([0, 0, 1, -1])[b[ys, xs]]
+        nx, ny = xs + dx, ys + dy
+        assert ((nx >= 0) & (nx < W) & (ny >= 0) & (ny < H)).all()
+        assert (cls[ny, nx] != orc.OBSTACLE).all()
+        free = np.argwhere(cls == 0)
+        sy, sx = free[int(rng.integers(0, len(free)))]
+        st1, c1 = orc.walk(cls, u, (int(sx), int(sy)), 4 * W * H)
+        st2, c2 = orc.walk_dir(m, (int(sx), int(sy)), 4 * W * H)
+        assert st1 == st2 and np.array_equal(c1, c2)

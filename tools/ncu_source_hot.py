@@ -47,3 +47,7 @@ print("all:", " ".join(f"{h[6:]}={v}" for h, v in tot_c.most_common(10) if v))
 for op in ("SYNCS.PHASECHK.TRANS64.TRYWAIT", "BRA", "LDS.128", "STG.E.128"):
     if op in agg:
         print(f"{op:30s}", " ".join(f"{h[6:]}={v}" for h, v in agg[op].most_common(5) if v))
+print("top instructions:")
+for n, a, s, r in sorted(recs, key=lambda x: -x[0])[:int(sys.argv[3]) if len(sys.argv) > 3 else 0]:
+    st = sorted(((int(r[idx[h]] or 0), h[6:]) for h in names if (r[idx[h]] or "0").isdigit()), reverse=True)[:3]
+    print(f"  {a[-5:]} {n:5d} {s[:60]:60s} {st}")
