@@ -161,6 +161,7 @@ static twg_status create_slab(const twg_grid_desc* d, int rank, int nranks, int3
 }
 
 TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stream, void* nccl_comm, twg_ctx** out) {
+    TWG_NVTX("twg_create");
     if (!d || !out) return fail(nullptr, TWG_E_INVALID_ARG, "null argument");
     *out = nullptr;
     if (!nccl_comm) return create_local(d, device, stream, out);
@@ -179,6 +180,7 @@ TWG_API twg_status twg_create(const twg_grid_desc* d, int32_t device, void* stre
 
 TWG_API twg_status twg_create_group(const twg_grid_desc* d, int32_t nslabs, int32_t device, void* stream,
                                     twg_ctx** out) {
+    TWG_NVTX("twg_create_group");
     if (!d || !out || nslabs < 1 || nslabs > kMaxLocalSlabs)
         return fail(nullptr, TWG_E_INVALID_ARG, "null argument or nslabs outside 1..16");
     cudaError_t e = cudaSetDevice(device);
@@ -203,6 +205,7 @@ TWG_API twg_status twg_create_group(const twg_grid_desc* d, int32_t nslabs, int3
 }
 
 TWG_API twg_status twg_slab_info(const twg_ctx* c, int32_t* out8) {
+    TWG_NVTX("twg_slab_info");
     if (!c || !out8) return TWG_E_INVALID_ARG;
     const bool sh = c->sharded();
     out8[0] = sh ? c->shard.rank : 0;
@@ -217,6 +220,7 @@ TWG_API twg_status twg_slab_info(const twg_ctx* c, int32_t* out8) {
 }
 
 TWG_API twg_status twg_destroy(twg_ctx* c) {
+    TWG_NVTX("twg_destroy");
     if (!c) return TWG_OK;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
@@ -240,6 +244,7 @@ TWG_API twg_status twg_destroy(twg_ctx* c) {
 }
 
 TWG_API twg_status twg_set_static(twg_ctx* c, int32_t b, const uint8_t* occ) {
+    TWG_NVTX("twg_set_static");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!occ || b < -1 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad scenario index or null mask");
@@ -277,6 +282,7 @@ TWG_API twg_status twg_set_static(twg_ctx* c, int32_t b, const uint8_t* occ) {
 
 TWG_API twg_status twg_set_obstacles(twg_ctx* c, int32_t b, const twg_robot* robot, int32_t goal_x, int32_t goal_y,
                                      const twg_track* tracks, int32_t n, const twg_warp_cfg* cfg, int32_t warm) {
+    TWG_NVTX("twg_set_obstacles");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!robot || b < 0 || b >= c->B || (n > 0 && !tracks)) return fail(c, TWG_E_INVALID_ARG, "bad argument");
@@ -295,6 +301,7 @@ TWG_API twg_status twg_set_obstacles(twg_ctx* c, int32_t b, const twg_robot* rob
 }
 
 TWG_API twg_status twg_relax(twg_ctx* c, const twg_relax_cfg* cfg, int32_t* sweeps_done, float* residual) {
+    TWG_NVTX("twg_relax");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     std::vector<int> part(c->B, 1);
@@ -303,6 +310,7 @@ TWG_API twg_status twg_relax(twg_ctx* c, const twg_relax_cfg* cfg, int32_t* swee
 
 TWG_API twg_status twg_extract_path(twg_ctx* c, int32_t b, const twg_band_cfg* cfg, int32_t* cells_xy,
                                     int32_t* n_cells, float* smooth_xy, int32_t* n_smooth, float* next_xy) {
+    TWG_NVTX("twg_extract_path");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad scenario index");
@@ -336,6 +344,7 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
                                  const twg_track* tracks, const int32_t* n_tracks, const twg_warp_cfg* warp,
                                  const twg_relax_cfg* rcfg, const twg_band_cfg* bcfg, twg_plan_result* out,
                                  int32_t* cells_xy, float* smooth_xy) {
+    TWG_NVTX("twg_plan_step");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!robot || !goal_xy || !rcfg || !bcfg || !out || b < -1 || b >= c->B)
@@ -356,13 +365,22 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
         bs.push_back(r.b);
     }
     if (off > 0 && !tracks && !resident) return fail(c, TWG_E_INVALID_ARG, "null tracks");
-    st = encode(c, reqs, tracks, warp, rcfg->warm_start, resident);
+    {
+        TWG_NVTX("twg_plan_step/encode");
+        st = encode(c, reqs, tracks, warp, rcfg->warm_start, resident);
+    }
     if (st != TWG_OK) return st;
     std::vector<int> part(c->B, 0);
     for (int q : bs) part[q] = 1;
-    st = relax(c, rcfg, part, nullptr, nullptr);
+    {
+        TWG_NVTX("twg_plan_step/relax");
+        st = relax(c, rcfg, part, nullptr, nullptr);
+    }
     if (st != TWG_OK) return st;
-    st = path(c, bs, bcfg);
+    {
+        TWG_NVTX("twg_plan_step/path");
+        st = path(c, bs, bcfg);
+    }
     if (st != TWG_OK) return st;
     // D2H: per scenario meta, sweeps, residual, flags (pinned staging), then the paths
     const int B = c->B;
@@ -431,6 +449,7 @@ TWG_API twg_status twg_plan_step(twg_ctx* c, int32_t b, const twg_robot* robot, 
 }
 
 TWG_API twg_status twg_get_field(twg_ctx* c, int32_t b, float* out, int32_t mode) {
+    TWG_NVTX("twg_get_field");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!out || b < 0 || b >= c->B || mode < 0 || mode > 2) return fail(c, TWG_E_INVALID_ARG, "bad argument");
@@ -453,6 +472,7 @@ TWG_API twg_status twg_get_field(twg_ctx* c, int32_t b, float* out, int32_t mode
 }
 
 TWG_API twg_status twg_set_field(twg_ctx* c, int32_t b, const float* raw) {
+    TWG_NVTX("twg_set_field");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!raw || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
@@ -477,6 +497,7 @@ TWG_API twg_status twg_set_field(twg_ctx* c, int32_t b, const float* raw) {
 }
 
 TWG_API twg_status twg_get_warp(twg_ctx* c, int32_t b, int32_t n, int32_t* t, int32_t* j, double* pred) {
+    TWG_NVTX("twg_get_warp");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (b < 0 || b >= c->B || n != c->scen[b].n_tracks) return fail(c, TWG_E_INVALID_ARG, "bad scenario or count");
@@ -490,6 +511,7 @@ TWG_API twg_status twg_get_warp(twg_ctx* c, int32_t b, int32_t n, int32_t* t, in
 }
 
 TWG_API twg_status twg_field_ptr(twg_ctx* c, int32_t b, void** dev_ptr, int64_t* pitch) {
+    TWG_NVTX("twg_field_ptr");
     if (!c || b < 0 || b >= c->B) return TWG_E_INVALID_ARG;
     if (dev_ptr) *dev_ptr = c->u[c->cur[b]] + (int64_t)b * c->sstride;
     if (pitch) *pitch = c->P;
@@ -497,6 +519,7 @@ TWG_API twg_status twg_field_ptr(twg_ctx* c, int32_t b, void** dev_ptr, int64_t*
 }
 
 TWG_API twg_status twg_debug_walk(twg_ctx* c, int32_t b, int32_t* out4) {
+    TWG_NVTX("twg_debug_walk");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!out4 || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
@@ -512,6 +535,7 @@ TWG_API twg_status twg_debug_walk(twg_ctx* c, int32_t b, int32_t* out4) {
 TWG_API int64_t twg_kernel_launches(const twg_ctx* c) { return c ? c->launches : 0; }
 
 TWG_API twg_status twg_profile(twg_ctx* c, int32_t enable) {
+    TWG_NVTX("twg_profile");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     TWG_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -524,6 +548,7 @@ TWG_API twg_status twg_profile(twg_ctx* c, int32_t enable) {
 }
 
 TWG_API twg_status twg_profile_read(twg_ctx* c, double* relax_ms, int64_t* relax_launches, int64_t* cell_sweeps) {
+    TWG_NVTX("twg_profile_read");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     TWG_CUDA(c, cudaStreamSynchronize(c->stream));

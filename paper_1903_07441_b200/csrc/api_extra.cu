@@ -12,6 +12,7 @@ using namespace twg::host;
 
 TWG_API twg_status twg_walk_from(twg_ctx* c, int32_t b, int32_t x, int32_t y, int32_t max_cells, int32_t* cells_xy,
                                  int32_t* n_cells, int32_t* code, int32_t* next_xy) {
+    TWG_NVTX("twg_walk_from");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (b < 0 || b >= c->B || x < 0 || x >= c->W || y < c->ghost || y >= c->H - c->ghost || max_cells < 0 || !code)
@@ -69,6 +70,7 @@ static twg_status index_matrix_core(twg_ctx* c, int32_t b) {
 
 TWG_API twg_status twg_band_index(twg_ctx* c, int32_t b, const twg_band_cfg* cfg, uint8_t* out, int32_t* cells_xy,
                                   int32_t* n_cells) {
+    TWG_NVTX("twg_band_index");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!cfg || b < 0 || b >= c->B || cfg->iterations < 0 || cfg->max_len < 1)
@@ -102,6 +104,7 @@ TWG_API twg_status twg_band_index(twg_ctx* c, int32_t b, const twg_band_cfg* cfg
 }
 
 TWG_API twg_status twg_index_matrix(twg_ctx* c, int32_t b, uint8_t* out) {
+    TWG_NVTX("twg_index_matrix");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!out || b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
@@ -115,6 +118,7 @@ TWG_API twg_status twg_index_matrix(twg_ctx* c, int32_t b, uint8_t* out) {
 }
 
 TWG_API twg_status twg_warp_map(twg_ctx* c, const twg_robot* robot, double warp_spacing, int32_t* out) {
+    TWG_NVTX("twg_warp_map");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!out || !robot || !(warp_spacing > 0.0)) return fail(c, TWG_E_INVALID_ARG, "bad argument");

@@ -3,9 +3,24 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX 3
+
 #include "twg_kernels.cuh"
 
+// NVTX range for the lifetime of a scope (one per C-ABI call and per phase of a plan step), so that
+// nsys / ncu --nvtx attribute device work to the call that enqueued it (tracing).
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+};
+#define TWG_NVTX_CAT2(a, b) a##b
+#define TWG_NVTX_CAT(a, b) TWG_NVTX_CAT2(a, b)
+#define TWG_NVTX(name) twg::host_nvtx::NvtxScope TWG_NVTX_CAT(twg_nvtx_, __LINE__)(name)
+
 namespace twg {
+namespace host_nvtx {
+using ::NvtxScope;
+}
 namespace host {
 
 extern std::string g_create_err;  // message of the last failed twg_create

@@ -104,6 +104,7 @@ SimArgs sim_args(twg_ctx* c, const twg_sim_cfg* f) {
 
 TWG_API twg_status twg_sim_reset(twg_ctx* c, int32_t b, const twg_robot* robot, int32_t goal_x, int32_t goal_y,
                                  const double* obstacles, int32_t n, const twg_sim_cfg* cfg) {
+    TWG_NVTX("twg_sim_reset");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!robot || b < 0 || b >= c->B || n < 0 || (n > 0 && !obstacles) || !sim_cfg_ok(cfg))
@@ -178,6 +179,7 @@ TWG_API twg_status twg_sim_reset(twg_ctx* c, int32_t b, const twg_robot* robot, 
 TWG_API twg_status twg_sim_tick(twg_ctx* c, const twg_sim_cfg* cfg, const twg_warp_cfg* warp,
                                 const twg_relax_cfg* rcfg, const twg_band_cfg* bcfg, const twg_tracker_cfg* tcfg,
                                 twg_sim_trial* out, int32_t* running) {
+    TWG_NVTX("twg_sim_tick");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!sim_cfg_ok(cfg) || !warp || !rcfg || !bcfg || !tcfg) return fail(c, TWG_E_INVALID_ARG, "bad argument");
@@ -255,6 +257,7 @@ TWG_API twg_status twg_sim_tick(twg_ctx* c, const twg_sim_cfg* cfg, const twg_wa
 }
 
 TWG_API twg_status twg_sim_histogram(twg_ctx* c, int32_t b, int32_t* hist) {
+    TWG_NVTX("twg_sim_histogram");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!hist || b < 0 || b >= c->B || !c->d_sim_hist) return fail(c, TWG_E_INVALID_ARG, "bad argument");

@@ -13,6 +13,7 @@ using namespace twg::host;
 
 TWG_API twg_status twg_track_update(twg_ctx* c, int32_t b, const double* det_xy, const int32_t* n_det,
                                     const twg_warp_cfg* wc, const twg_tracker_cfg* cfg, int32_t* n_tracks) {
+    TWG_NVTX("twg_track_update");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (!n_det || !wc || !cfg || b < -1 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad argument");
@@ -65,6 +66,7 @@ TWG_API twg_status twg_track_update(twg_ctx* c, int32_t b, const double* det_xy,
 }
 
 TWG_API twg_status twg_get_tracks(twg_ctx* c, int32_t b, twg_track* out, int32_t* missed, int32_t cap, int32_t* n) {
+    TWG_NVTX("twg_get_tracks");
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (b < 0 || b >= c->B || cap < 0) return fail(c, TWG_E_INVALID_ARG, "bad argument");
