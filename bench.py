@@ -290,10 +290,13 @@ def run_ours(args):
     T_eff = rcells / rl / cells if rl else 0
     bytes_per_launch = 8.0 * cells  # one fp32 read + one fp32 write per cell per launch
     achieved = bytes_per_launch / avg_launch_s / 1e9
-    traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum of one launch, from the committed ncu capture
-    tp = os.path.join(ROOT, "profiles", "r01_relax_traffic.json")
-    if os.path.exists(tp) and N == 4096:
-        traffic = json.load(open(tp)).get("traffic_bytes_per_launch")
+    # dram__bytes_read.sum + dram__bytes_write.sum of one T = 6 launch at 4096^2: not measured in this run
+    # (ncu replays kernels), read from the newest committed `ncu --set full` capture and labelled so
+    traffic, traffic_src = None, None
+    caps = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_relax_traffic.json"))
+    if caps and N == 4096:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", caps[-1]))).get("traffic_bytes_per_launch")
+        traffic_src = f"committed ncu capture profiles/{caps[-1]} (not measured in this run)"
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -306,7 +309,10 @@ def run_ours(args):
         "plan_steps_per_s": args.steps * ws / (ms * 1e-3),
         "relax_glups": cells * args.relax_sweeps / (relax_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_rb_tblock", "bytes_per_launch": bytes_per_launch,
+                     "traffic": traffic, "traffic_source": traffic_src, "kernel": "k_rb_tblock",
+                     "bytes_per_launch": bytes_per_launch,
+                     "relax_glups_pct_of_8B_roofline": 100.0 * (cells * args.relax_sweeps / (relax_ms * 1e-3) / 1e9) /
+                                                       (peak / 8.0),
                      "sweeps_per_launch": T_eff, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,
                      "launches_per_step": rl / args.steps if rl else None,
                      "kernel_share_of_step": (rms / ms_prof) if ms_prof else None,
@@ -324,6 +330,9 @@ def run_ours(args):
         # that the driver's 1/2/4/8 runs carry their scaling too
         out["c4_slab"] = c4_slab(args, dev, ws, rank, local)
         out["c5_batch"] = c5_batch(args, dev, ws, rank, local)
+        if rank == 0:  # single-GPU configurations (BASELINE configs[0], [1])
+            out["c1_solve"] = c1_solve(args, dev, not args.no_cpu_baseline)
+            out["c2_loop"] = c2_loop(args, dev, not args.no_cpu_baseline)
     if rank == 0 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
@@ -340,6 +349,91 @@ def run_ours(args):
     pl.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------- C1, C2 sub-results
+def c1_solve(args, dev, with_oracle):
+    """BASELINE configs[0]: 64^2, one static disk, cold relaxation to residual 1e-6 (check every sweep)
+    and path extraction: time to tolerance on the GPU (CUDA events) and for the oracle (one core)."""
+    import torch
+    from paper_1903_07441_b200 import Planner, band_cfg, relax_cfg, warp_cfg
+    from scenes import scene_c1
+    sc = scene_c1()
+    stream = torch.cuda.current_stream(dev)
+    pl = Planner(sc.W, sc.H, 1, sc.cell_size, sc.origin, device=dev.index, stream=stream.cuda_stream)
+    pl.set_static(sc.static)
+    rc = relax_cfg(max_sweeps=10 ** 6, check_every=1, tol=1e-6, warm_start=0)
+    bc = band_cfg(50, 1000, 4000)
+    best, sweeps = 1e9, None
+    for _ in range(3):
+        pl.set_obstacles(0, sc.robot, sc.goal, sc.tracks, warp_cfg(), warm=0)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sw, _ = pl.relax(rc)
+        pl.extract_path(0, bc)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        best, sweeps = min(best, e0.elapsed_time(e1)), int(sw[0])
+    pl.close()
+    out = {"workload": "c1_64: cold relax to residual 1e-6 (check every sweep) + walk + 50 band iterations",
+           "sweeps": sweeps, "gpu_ms": best}
+    if with_oracle:
+        import oracle
+        t0 = time.perf_counter()
+        ref = oracle.plan_step(sc, max_sweeps=10 ** 6, check_every=1, tol=1e-6, iters=50, max_len=1000)
+        out.update(oracle_ms=1e3 * (time.perf_counter() - t0), oracle_cores=1, oracle_sweeps=ref["sweeps"])
+    return out
+
+
+def c2_loop(args, dev, with_oracle):
+    """BASELINE configs[1]: 512^2, 20 obstacles, the warm plan loop (S = 100, I = 50) after a tick-0
+    solve to the exact fp32 fixed point: plan steps/s on the GPU (device-resident tracks, CUDA events)
+    and for the oracle (its OpenMP variants on every host core)."""
+    import torch
+    from paper_1903_07441_b200 import Planner, band_cfg, relax_cfg, warp_cfg
+    from scenes import advance_scene, scene_c2
+    sc0 = scene_c2(0)
+    stream = torch.cuda.current_stream(dev)
+    pl = Planner(sc0.W, sc0.H, 1, sc0.cell_size, sc0.origin, device=dev.index, stream=stream.cuda_stream)
+    pl.set_static(sc0.static)
+    wc, bc = warp_cfg(), band_cfg(args.band_iters, 4096, 8192)
+    pl.plan_step(0, [sc0.robot], [sc0.goal], sc0.tracks, [sc0.n_tracks], wc,
+                 relax_cfg(max_sweeps=400000, check_every=1000, tol=1e-38, warm_start=0, sync_every=8), bc,
+                 want_paths=False)
+    n = args.warmup + args.steps
+    scs = [advance_scene(sc0, 1 + k) for k in range(n)]
+    dtr = [torch.from_numpy(np.ascontiguousarray(s.tracks)).to(dev) for s in scs]
+    rc = relax_cfg(max_sweeps=args.sweeps, warm_start=1)
+    for k in range(args.warmup):
+        pl.plan_step(0, [scs[k].robot], [scs[k].goal], dtr[k], [scs[k].n_tracks], wc, rc, bc, want_paths=False)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ok = 0
+    e0.record(stream)
+    for k in range(args.warmup, n):
+        _, r, _, _ = pl.plan_step(0, [scs[k].robot], [scs[k].goal], dtr[k], [scs[k].n_tracks], wc, rc, bc,
+                                  want_paths=False)
+        ok += int(r[0].walk_status == 0)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    pl.close()
+    out = {"workload": f"c2_512: warm plan step S={args.sweeps}, I={args.band_iters}, 20 obstacles, after a tick-0 "
+                       f"solve to the fp32 fixed point", "plan_steps_per_s": args.steps / (ms * 1e-3),
+           "glups": 512 * 512 * args.sweeps * args.steps / (ms * 1e-3) / 1e9, "walk_ok_steps": ok,
+           "steps": args.steps}
+    if with_oracle:
+        import oracle
+        cores = oracle.host_cores()
+        r0 = oracle.plan_step(sc0, max_sweeps=400000, check_every=1000, tol=1e-38, iters=args.band_iters,
+                              max_len=4096, threads=cores)
+        t0, prev = time.perf_counter(), r0
+        for k in range(2):
+            prev = oracle.plan_step(scs[k], max_sweeps=args.sweeps, iters=args.band_iters, max_len=4096, prev=prev,
+                                    threads=cores)
+        out.update(oracle_plan_steps_per_s=2 / (time.perf_counter() - t0), oracle_cores=cores)
+    return out
 
 
 # ---------------------------------------------------------------------------- C4: row slabs
@@ -445,7 +539,9 @@ def c5_batch(args, dev, ws, rank, local):
     for k in range(1 + args.warmup + args.steps):
         inputs(k)
     t_prep = time.perf_counter()
-    step(0, relax_cfg(max_sweeps=100000, check_every=2000, tol=1e-38, warm_start=0, sync_every=4))
+    # tick 0: cold solve to the fp32 fixed point; scenes whose cold field drains slowly through narrow
+    # passages stop at the cap (profiles/r02_c5_nopath.json)
+    step(0, relax_cfg(max_sweeps=300000, check_every=2000, tol=1e-38, warm_start=0, sync_every=4))
     prep_s = time.perf_counter() - t_prep
     rc = relax_cfg(max_sweeps=args.sweeps, warm_start=1)
     for k in range(args.warmup):

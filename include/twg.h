@@ -90,9 +90,11 @@ enum {
  *    [G, height - G)).
  * With G > 0 the residual of twg_relax covers the owned rows only, the goal
  * and the robot may lie outside the local grid (their cells are then simply
- * absent), and twg_extract_path / twg_plan_step are not available (the walk
- * is handed over between slabs with twg_walk_from).  Single-GPU contexts pass
- * 0 for row_offset, ghost_rows and exchange_every. */
+ * absent) and twg_plan_step is not available; twg_extract_path works on
+ * sharded contexts (the walk is handed over between the slabs and every slab
+ * returns the whole path in global cells, see twg_extract_path) but not on
+ * manual slabs (hand the walk over with twg_walk_from).  Single-GPU contexts
+ * pass 0 for row_offset, ghost_rows and exchange_every. */
 typedef struct {
     int32_t width, height, batch, row_offset;
     int32_t ghost_rows, exchange_every;
@@ -318,7 +320,14 @@ TWG_API twg_status twg_relax(twg_ctx* ctx, const twg_relax_cfg* cfg, int32_t* sw
  *      resampling (C15) into smooth_xy (max_smooth (x, y) float pairs);
  *   a9 next waypoint into next_xy[2] (cell units).
  * Host arrays; any output pointer may be NULL.  Returns OK, W_TRUNCATED or
- * NO_PATH (then *n_cells = *n_smooth = 0 and next_xy = robot cell centre). */
+ * NO_PATH (then *n_cells = *n_smooth = 0 and next_xy = robot cell centre).
+ * Sharded contexts (b = 0; every slab of the group calls it, NCCL ranks
+ * collectively): the walk runs on the slab owning the current cell and is
+ * handed to the neighbouring slab when it steps into a ghost row (ncclBroadcast
+ * of the walker state); the band and the resampling run on the rows of the
+ * global grid within I step sqrt(2) + 3 of the path, assembled from the slabs
+ * (SURVEY 8(e)); cells, smooth points and next waypoint are in global
+ * coordinates and identical on every slab. */
 TWG_API twg_status twg_extract_path(twg_ctx* ctx, int32_t b, const twg_band_cfg* cfg,
                                     int32_t* cells_xy, int32_t* n_cells,
                                     float* smooth_xy, int32_t* n_smooth, float* next_xy);

@@ -8,7 +8,7 @@ import sys
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_HERE)
 SOURCES = ["api.cu", "api_track.cu", "api_sim.cu", "api_extra.cu", "host_core.cu", "k_relax.cu", "k_stamp.cu",
-           "k_path.cu", "k_track.cu", "k_sim.cu", "nccl_link.cu"]
+           "k_path.cu", "k_track.cu", "k_sim.cu", "nccl_link.cu", "api_shard.cu"]
 HEADERS = ["twg_internal.cuh", "twg_kernels.cuh", "api_host.cuh"]
 OUT = os.path.join(_HERE, "libtwg.so")
 

@@ -314,7 +314,12 @@ TWG_API twg_status twg_extract_path(twg_ctx* c, int32_t b, const twg_band_cfg* c
     twg_status st = check_ctx(c);
     if (st != TWG_OK) return st;
     if (b < 0 || b >= c->B) return fail(c, TWG_E_INVALID_ARG, "bad scenario index");
-    if (c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "path extraction is not available on a row slab");
+    if (c->sharded()) {
+        if (!cfg || cfg->max_len < 1 || cfg->max_smooth < 1 || cfg->iterations < 0 || cfg->iterations > 6000)
+            return fail(c, TWG_E_INVALID_ARG, "band cfg: max_len, max_smooth >= 1, 0 <= iterations <= 6000");
+        return sharded_extract_path(c, cfg, cells_xy, n_cells, smooth_xy, n_smooth, next_xy);
+    }
+    if (c->ghost > 0) return fail(c, TWG_E_INVALID_ARG, "path extraction is not available on a manual row slab");
     st = path(c, {b}, cfg);
     if (st != TWG_OK) return st;
     PathMeta* hm = nullptr;

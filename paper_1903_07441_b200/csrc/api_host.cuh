@@ -78,6 +78,11 @@ twg_status nccl_exchange(twg_ctx* c, size_t cnt, int up, int dn, const float* s_
                          float* r_dn, cudaStream_t st);
 twg_status nccl_allreduce_max_u32(twg_ctx* c, unsigned* buf, int n, cudaStream_t st);
 twg_status nccl_bcast_i32(twg_ctx* c, int* buf, int n, int root, cudaStream_t st);
+twg_status nccl_allreduce_sum_u32(twg_ctx* c, unsigned* buf, size_t n, cudaStream_t st);
+// Rows a7-a9 on a row-slab group (api_shard.cu): walk handed over between the slabs, then the band on
+// the gathered corridor rows; every slab returns the whole path (global cells).
+twg_status sharded_extract_path(twg_ctx* c, const twg_band_cfg* cfg, int32_t* cells_xy, int32_t* n_cells,
+                                float* smooth_xy, int32_t* n_smooth, float* next_xy);
 // Rows a7-a9 for a list of scenarios (results stay on the device).
 twg_status path(twg_ctx* c, const std::vector<int>& bs, const twg_band_cfg* cfg);
 // Row f1 tick for the requests rq (det_off relative to `det`, a device array of (x, y) pairs).

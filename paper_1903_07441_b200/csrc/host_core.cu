@@ -346,6 +346,8 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
         sc.gy = ps[k].gy;
         sc.rcx = ps[k].rcx;
         sc.rcy = ps[k].rcy;
+        sc.rx = reqs[k].robot.x;
+        sc.ry = reqs[k].robot.y;
         sc.n_tracks = reqs[k].n;
         if (!resident) sc.trk_n = reqs[k].n;
         sc.n_boxes = reqs[k].n;

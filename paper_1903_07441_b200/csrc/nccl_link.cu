@@ -130,6 +130,11 @@ twg_status nccl_allreduce_max_u32(twg_ctx* c, unsigned* buf, int n, cudaStream_t
     return TWG_OK;
 }
 
+twg_status nccl_allreduce_sum_u32(twg_ctx* c, unsigned* buf, size_t n, cudaStream_t st) {
+    TWG_NCCL(c, g_fns.allReduce(buf, buf, n, kNcclUint32, 0 /* ncclSum */, c->shard.nccl, st));
+    return TWG_OK;
+}
+
 twg_status nccl_bcast_i32(twg_ctx* c, int* buf, int n, int root, cudaStream_t st) {
     TWG_NCCL(c, g_fns.broadcast(buf, buf, (size_t)n, kNcclInt32, root, c->shard.nccl, st));
     return TWG_OK;

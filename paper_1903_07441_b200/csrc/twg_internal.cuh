@@ -212,6 +212,7 @@ struct twg_ctx {
     // encode state
     struct Scen {
         int gx = -1, gy = -1, rcx = -1, rcy = -1;
+        double rx = 0.0, ry = 0.0;  // robot position of the last encode (m): the global robot cell of a slab
         int n_tracks = 0, n_boxes = 0;
         int trk_n = 0;  // tracks in the resident tracker table (row f1)
         bool encoded = false, static_dirty = true;

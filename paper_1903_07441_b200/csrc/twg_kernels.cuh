@@ -125,6 +125,10 @@ struct PathArgs {
     int spec_on;           // speculative segment walkers (markers in k_index_dir / k_walk / k_spec_stitch)
 };
 cudaError_t launch_path(const PathArgs& p, int* n_launch, cudaStream_t st);
+cudaError_t launch_band_resample(const PathArgs& p, cudaStream_t st);  // a8-a9 after a walk (2 launches)
+cudaError_t launch_seg_append(const int* seg, const int* wout, int row_off, int at, int2* path, int* msg,
+                              cudaStream_t st);
+cudaError_t launch_cells_shift(const int2* in, int n, int dy, int2* out, cudaStream_t st);
 cudaError_t launch_index_dir(const PathArgs& p, cudaStream_t st);  // k_index_dir alone (twg_index_matrix)
 // f3 per-cell band on the index matrix (2 iters launches) and the walk along a matrix
 cudaError_t launch_cellband(const float* f, int64_t P, int W, int H, uint8_t* dir, int iters, float kt, int* n_launch,

@@ -13,7 +13,8 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import oracle  # noqa: E402
-from paper_1903_07441_b200 import Planner, relax_cfg, warp_cfg  # noqa: E402
+from paper_1903_07441_b200 import Planner, band_cfg, relax_cfg, warp_cfg  # noqa: E402
+from paper_1903_07441_b200 import twg as T  # noqa: E402
 from paper_1903_07441_b200.slab import (SlabLayout, TwgSlabBackend, make_group, make_sharded, nccl_comm_for,  # noqa: E402
                                         owned_rows, sharded_walk_local, WALK_GOAL)
 from paper_1903_07441_b200.twg import nccl_comm_destroy  # noqa: E402
@@ -98,5 +99,46 @@ def test_nccl_slab_world_size_1(k, S, check_every, tol):
     s, res = pl.relax(relax_cfg(max_sweeps=S, check_every=check_every, tol=tol))
     assert int(s[0]) == sw and np.float32(res[0]) == np.float32(rs)
     assert np.array_equal(owned_rows(pl).view(np.uint32), ref.view(np.uint32))
+    pl.close()
+    nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("nslabs,k,iters", [(3, 6, 50), (4, 4, 20)])
+def test_group_extract_path_equals_single_grid(nslabs, k, iters):
+    # twg_extract_path on a local slab group: walk handed over between the slabs, band + resampling on
+    # the gathered corridor -- cells, smoothed path and next waypoint bit-identical to the oracle's
+    # single-grid plan step (every slab returns the same global path)
+    sc = scene_random("gpath", 150, 4, 6, 8)
+    st = torch.cuda.current_stream().cuda_stream
+    S = 20000
+    pls = make_group(sc.W, sc.H, nslabs, sc.static, sc.robot, sc.goal, sc.tracks, warp_cfg(), k, stream=st)
+    pls[0].relax(relax_cfg(max_sweeps=S))
+    ref = oracle.plan_step(sc, max_sweeps=S, iters=iters, max_len=4000)
+    assert ref["walk_status"] == oracle.OK
+    owners = {next(r for r, p in enumerate(pls) if p.r0 <= y < p.r1) for _, y in ref["cells"]}
+    assert len(owners) > 1  # the walk crosses slabs
+    for p in (pls[0], pls[-1]):
+        s, cells, sm, ns, nxt = p.extract_path(0, band_cfg(iters, 4000, 8000))
+        assert s == T.OK
+        assert np.array_equal(cells, ref["cells"])
+        assert np.array_equal(sm.view(np.uint32), ref["smooth"].view(np.uint32))
+        assert nxt == ref["next"]
+    for p in pls:
+        p.close()
+
+
+def test_nccl_slab_extract_path_world_size_1():
+    sc = scene_random("npath", 128, 3, 6, 8)
+    S = 20000
+    comm = nccl_comm_for(0, 1, 0)
+    st = torch.cuda.current_stream().cuda_stream
+    pl = make_sharded(sc.W, sc.H, sc.static, sc.robot, sc.goal, sc.tracks, warp_cfg(), 6, comm, stream=st)
+    pl.relax(relax_cfg(max_sweeps=S))
+    ref = oracle.plan_step(sc, max_sweeps=S, iters=50, max_len=4000)
+    s, cells, sm, ns, nxt = pl.extract_path(0, band_cfg(50, 4000, 8000))
+    assert (s == T.OK) == (ref["walk_status"] == oracle.OK)
+    if s == T.OK:
+        assert np.array_equal(cells, ref["cells"])
+        assert np.array_equal(sm.view(np.uint32), ref["smooth"].view(np.uint32)) and nxt == ref["next"]
     pl.close()
     nccl_comm_destroy(comm)
