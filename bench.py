@@ -484,6 +484,16 @@ def c4_slab(args, dev, ws, rank, local):
            "gpu_launches": int(launches), "residual_after": float(res[0])}
     pl.close()
     nccl_comm_destroy(comm)
+    if rank == 0 and not args.no_cpu_baseline:  # the oracle at S = 8 (every host core)
+        import oracle
+        _, cls, *_ = oracle.classify(sc)
+        u = oracle.init_u32(cls)
+        cores = oracle.host_cores()
+        t0 = time.perf_counter()
+        oracle.relax_f32(cls, u, 8, 8, 0.0, threads=cores)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": sc.W * sc.H * 8 / dt / 1e9, "unit": "GLUP/s", "cores": cores, "kind": "oracle",
+                               "sample": f"8 red-black sweeps of the whole 16384^2 grid, {dt:.2f} s"}
     return out
 
 
@@ -590,6 +600,21 @@ def c5_batch(args, dev, ws, rank, local):
            "walk_ok_fraction": ok / (args.steps * per * ws), "status_counts_rank0": status, "prep_s": prep_s,
            "results_gathered": gathered, "gpu_launches": int(launches)}
     pl.close()
+    if rank == 0 and not args.no_cpu_baseline:  # the oracle's scenario-steps/s on a sample of the scenarios
+        import oracle
+        cores = oracle.host_cores()
+        dt, n = 0.0, 0
+        for sc in scs[:4]:  # tick 0 (untimed, 20 000 sweeps) then two timed warm steps each
+            prev = oracle.plan_step(advance_scene(sc, 0), max_sweeps=20000, check_every=2000, tol=1e-38,
+                                    iters=args.band_iters, max_len=4096, threads=cores)
+            for k in range(2):
+                t0 = time.perf_counter()
+                prev = oracle.plan_step(advance_scene(sc, 1 + k), max_sweeps=args.sweeps, iters=args.band_iters,
+                                        max_len=4096, prev=prev, threads=cores)
+                dt += time.perf_counter() - t0
+                n += 1
+        out["cpu_baseline"] = {"value": n / dt, "unit": "scenario-steps/s", "cores": cores, "kind": "oracle",
+                               "sample": f"{n} warm oracle plan steps of C5 scenes (S={args.sweeps}, I={args.band_iters})"}
     return out
 
 

@@ -36,14 +36,16 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every translation unit in parallel (one nvcc per file), then link libtwg.so."""
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile every translation unit in parallel (one nvcc per file), then link libtwg.so (or `out`, with
+    extra -D `defines`: variant builds for timing experiments)."""
+    OUT = out or globals()["OUT"]
+    if out is None and not force and not needs_build():
         return OUT
     from concurrent.futures import ThreadPoolExecutor
     import tempfile
     inc = ["-I", os.path.join(ROOT, "include")]
-    comp = [f for f in NVCC_FLAGS if f != "-shared"]
+    comp = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
     with tempfile.TemporaryDirectory(prefix="twg_build_") as tmp:
         objs = [os.path.join(tmp, os.path.splitext(s)[0] + ".o") for s in SOURCES]
 

@@ -24,7 +24,10 @@ namespace twg {
 // (DESIGN.md "k_rb_tblock").
 constexpr int kWarpsPerCta = 4;
 constexpr int kStripW = 128;
-constexpr int kStages = 2;
+#ifndef TWG_RELAX_STAGES
+#define TWG_RELAX_STAGES 2
+#endif
+constexpr int kStages = TWG_RELAX_STAGES;
 constexpr int kMaxT = 8;
 constexpr int kMaxLocalSlabs = 16;  // slabs of one local row-slab group
 

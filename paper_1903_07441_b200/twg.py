@@ -15,6 +15,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtwg.so")
+# TWG_LIB_PATH: an alternative build of the same library (kernel-variant timing experiments, tools/)
+LIB_PATH = os.environ.get("TWG_LIB_PATH") or LIB_PATH
 
 OK, W_GOAL_SWALLOWED, W_TRUNCATED = 0, 1, 2
 E_INVALID_ARG, E_OUT_OF_BOUNDS, E_OVERLAPPING_CLASSES, E_INVALID_START = -1, -2, -3, -4
