@@ -83,6 +83,7 @@ __device__ __forceinline__ void wave_step(float4 (&win)[2 * T + 2], int i, unsig
     }
     constexpr int so = (S - 2 * T + 2 * NW) % NW;
     if (lane_out && (unsigned)(i - 4 * T) < hs) *reinterpret_cast<float4*>(op) = win[so];
+    TWG_CHECK(!(lane_out && (unsigned)(i - 4 * T) < hs) || (unsigned)(i - 4 * T) < hs);
     op += P;
 }
 
@@ -100,6 +101,7 @@ struct Strip {
     // packed fast path near the goal (GOAL variant): the goal's absolute row, lane, column parity of its
     // pair (0: a, 1: b) and element; ystart = absolute row of step 0
     int ystart, gy, gl, gp, ge;
+    int y0, row_lo, row_hi, x, P_cols;  // checked build: the stored rows and columns must lie in the grid
 };
 
 // Steps S, S+1, ..., NW-1 of one unrolled block of the row loop.  S is a template parameter so
@@ -252,6 +254,8 @@ __device__ __forceinline__ void fast_store(FRow (&win)[2 * T + 2], int i, Strip&
     const FRow& w = win[so];
     const float4 o =
         make_float4(enc_of(w.a.x, w.ma.x), enc_of(w.b.x, w.mb.x), enc_of(w.a.y, w.ma.y), enc_of(w.b.y, w.mb.y));
+    TWG_CHECK(!(st.lane_out && (unsigned)(i - 4 * T) < st.hs) ||
+              (st.y0 + i - 4 * T >= st.row_lo && st.y0 + i - 4 * T < st.row_hi && st.x + 3 < st.P_cols));
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\n@p st.global.v4.f32 [%0], {%1, %2, %3, %4};\n}" ::"l"(st.op),
                  "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w), "r"((st.lane_out && (unsigned)(i - 4 * T) < st.hs) ? 1 : 0));
     st.op += st.P;
@@ -354,6 +358,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     const int nblk = (hs + 4 * T + NW - 1) / NW;  // rows ystart .. ystart + nblk*NW - 1
     st.lane = lane;
     st.P = a.P;
+    st.y0 = y0;
+    st.row_lo = a.row_lo;
+    st.row_hi = a.row_hi;
+    st.P_cols = (int)a.P;
 
     extern __shared__ __align__(128) unsigned char smem[];
     float* ring = reinterpret_cast<float*>(smem) + warp * (kStages * STAGE_F);
@@ -372,6 +380,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
 
     const int x = xb + 4 * lane;
     st.lane_out = lane >= HX / 4 && lane < 32 - HX / 4 && x < a.W;
+    st.x = x;
+    TWG_CHECK(y0 >= a.row_lo && y0 < a.row_hi && hs > 0);
     // row i - 4T of the segment is finalised at step i: start 4T rows above the first output row
     st.op = (src ? a.u0 : a.u1) + (int64_t)b * a.sstride + (int64_t)(y0 - 4 * T) * a.P + x;
     st.dmax = 0.0f;

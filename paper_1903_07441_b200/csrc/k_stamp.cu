@@ -46,6 +46,7 @@ __global__ void k_unstamp(EncodeArgs e) {
     const uint8_t* m = e.mask + (int64_t)b * e.H * e.W;
     for (int q = threadIdx.x; q < n; q += blockDim.x) {
         const int x = bx.x + q % nx, y = bx.z + q / nx;
+        TWG_CHECK(x >= 0 && x < e.W && y >= 0 && y < e.H);
         float* p = f + (int64_t)y * e.P + x;
         if (__float_as_uint(*p) == 0u && m[(int64_t)y * e.W + x] == 0) *p = -0.0f;  // free, u = 0
     }
@@ -211,6 +212,7 @@ __global__ void k_stamp(EncodeArgs e) {
         const double cy = e.oy + ((double)k + 0.5) * e.cs;
         const double ddx = cx - xp, ddy = cy - yp;
         if (ddx * ddx + ddy * ddy <= R2) {
+            TWG_CHECK(i >= 0 && i < e.W && k >= 0 && k < e.H);
             if (i == sp.gx && k == sp.gy) {
                 atomicOr(&e.flags[b], 1);  // TWG_W_GOAL_SWALLOWED: the goal is kept
             } else if (!(i == sp.rcx && k == sp.rcy)) {

@@ -185,6 +185,24 @@ inline bool first_on_device(unsigned long long& mask) {
 
 __device__ __forceinline__ bool is_free(float v) { return __float_as_int(v) < 0; }
 
+// Device-side bounds checks of the checked build (-DTWG_CHECKED, tests/test_gpu_checked.py): the
+// substitute for compute-sanitizer's memcheck where the GPU pool does not run it.  A failed check
+// prints its location and traps (the launch fails with cudaErrorLaunchFailure); compiled out otherwise.
+#ifdef TWG_CHECKED
+#define TWG_CHECK(cond)                                                                                   \
+    do {                                                                                                  \
+        if (!(cond)) {                                                                                    \
+            printf("TWG_CHECK failed: %s at %s:%d (block %d,%d thread %d)\n", #cond, __FILE__, __LINE__,  \
+                   (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                                    \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define TWG_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 }  // namespace twg
 
 // ---------------------------------------------------------------- context
