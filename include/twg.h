@@ -142,6 +142,9 @@ typedef struct {
  *   max_sweeps (C5); stop early when it is < tol (tol <= 0: fixed budget,
  *   C6); warm_start [1]: used by twg_plan_step's encode (C7);
  *   temporal_depth [0 = auto = 6]: sweeps fused per tile load (T, 1..8);
+ *   with both temporal_depth and rows_per_warp 0, a grid of at most 40960
+ *   cells is solved by one CTA per scenario in shared memory (all sweeps,
+ *   the residual and the stop rule in one launch; same result);
  *   rows_per_warp [0 = auto, load model of DESIGN.md]: rows of the strip one
  *   warp owns;
  *   sync_every [64]: convergence flags are read back every sync_every

@@ -621,7 +621,29 @@ twg_status relax_group(const std::vector<twg_ctx*>& g, const twg_relax_cfg* cfg,
     }
 
     int lp = 0;  // launches so far (parity)
-    if (maxs > 0) {
+    bool maxs_done_small = false;
+    static const bool no_small = [] { const char* e = std::getenv("TWG_NO_SMALL"); return e && e[0] == '1'; }();
+    // (an explicit temporal_depth / rows_per_warp asks for the tile kernel)
+    if (maxs > 0 && !sh && !jacobi && !lex && !no_small && cfg->temporal_depth == 0 && cfg->rows_per_warp == 0 &&
+        small_grid(c0->W, c0->H)) {
+        // one CTA per scenario solves the whole relaxation in shared memory (k_rb_small), in place
+        RelaxArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.u0 = c0->u[0];
+        a.u1 = c0->u[1];
+        a.cur = c0->d_cur;
+        a.P = c0->P;
+        a.sstride = c0->sstride;
+        a.W = c0->W;
+        a.H = c0->H;
+        a.done = c0->d_done;
+        a.res_r0 = c0->ghost;
+        a.res_r1 = c0->H - c0->ghost;
+        TWG_CUDA(c0, launch_rb_small(a, B, maxs, check, tol, c0->row_off & 1, c0->d_sweeps, c0->d_res, ms));
+        c0->launches += 1;
+        maxs_done_small = true;
+    }
+    if (maxs > 0 && !maxs_done_small) {
         int done_sw = 0, nchunk = 0;
         int lex_base = 0;  // sweeps finished by earlier lexicographic launches of this call
         while (done_sw < maxs) {

@@ -432,6 +432,97 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
     }
 }
 
+// ---------------------------------------------------------------- small grids: one CTA, whole solve
+// Grids whose field fits in shared memory (W H <= kSmallCells, e.g. C1's 64^2) are relaxed by one CTA
+// per scenario in a single launch: the field is staged in shared memory, every half-sweep is a block-
+// wide pass over one colour (in place: cells of one colour never neighbour each other) separated by
+// barriers, and the residual (max |du| of the sweep's free cells, C5) and the stop rule (C6) are
+// evaluated on the device after every check sweep -- the same operations as the tile kernel and the
+// oracle, without one launch (plus one k_check) per chunk.  The result is written back in place.
+constexpr int kSmallCells = 40960;  // 160 KiB of shared memory
+constexpr int kSmallThreads = 1024;
+
+__global__ void __launch_bounds__(kSmallThreads) k_rb_small(RelaxArgs a, int max_sweeps, int check_every, float tol,
+                                                            int qoff, int* __restrict__ sweeps_out,
+                                                            float* __restrict__ res_out) {
+    extern __shared__ float sf[];  // [H][W]
+    __shared__ unsigned s_red[32];
+    __shared__ int s_stop;
+    pdl_wait();
+    pdl_trigger();
+    const int b = blockIdx.x;
+    if (a.done[b]) return;
+    const int W = a.W, H = a.H, n = W * H;
+    float* g = (a.cur[b] ? a.u1 : a.u0) + (int64_t)b * a.sstride;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) sf[q] = g[(int64_t)(q / W) * a.P + q % W];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float res = 0.0f;
+    int s = 0;
+    for (s = 1; s <= max_sweeps; ++s) {
+        const bool check = (s % check_every == 0) || s == max_sweeps;
+        float dmax = 0.0f;
+        for (int color = 0; color < 2; ++color) {
+            // cells of this colour: (x + row_offset + y) & 1 == color, i.e. x = 2 j + ((color + qoff + y) & 1)
+            const int half = (W + 1) / 2;
+            for (int t = threadIdx.x; t < half * H; t += blockDim.x) {
+                const int y = t / half;
+                const int x = 2 * (t - y * half) + ((color + qoff + y) & 1);
+                if (x >= W) continue;
+                const int q = y * W + x;
+                const float c = sf[q];
+                if (!is_free(c)) continue;
+                const float e = x + 1 < W ? fabsf(sf[q + 1]) : 0.0f;
+                const float w = x > 0 ? fabsf(sf[q - 1]) : 0.0f;
+                const float nn = y > 0 ? fabsf(sf[q - W]) : 0.0f;
+                const float ss = y + 1 < H ? fabsf(sf[q + W]) : 0.0f;
+                const float nv = 0.25f * ((e + w) + (nn + ss));
+                if (check && y >= a.res_r0 && y < a.res_r1) dmax = fmaxf(dmax, fabsf(-nv - c));
+                sf[q] = -nv;
+            }
+            __syncthreads();
+        }
+        if (check) {
+            unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(dmax));
+            if (lane == 0) s_red[wid] = m;
+            __syncthreads();
+            if (wid == 0) {
+                m = lane < (int)(blockDim.x >> 5) ? s_red[lane] : 0u;
+                m = __reduce_max_sync(0xffffffffu, m);
+                if (lane == 0) {
+                    res = __uint_as_float(m);
+                    s_stop = ((s % check_every == 0 && res < tol) || s == max_sweeps) ? 1 : 0;
+                    s_red[0] = m;
+                }
+            }
+            __syncthreads();
+            res = __uint_as_float(s_red[0]);
+            if (s_stop) break;
+            __syncthreads();  // s_red / s_stop are rewritten at the next check
+        }
+    }
+    if (s > max_sweeps) s = max_sweeps;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) g[(int64_t)(q / W) * a.P + q % W] = sf[q];
+    if (threadIdx.x == 0) {
+        sweeps_out[b] = s;
+        res_out[b] = res;
+    }
+}
+
+bool small_grid(int W, int H) { return (int64_t)W * H <= kSmallCells; }
+
+cudaError_t launch_rb_small(const RelaxArgs& a, int B, int max_sweeps, int check_every, float tol, int qoff,
+                            int* sweeps_out, float* res_out, cudaStream_t st) {
+    const size_t smem = (size_t)a.W * a.H * sizeof(float);
+    static unsigned long long attr_mask = 0;
+    if (first_on_device(attr_mask))
+        cudaFuncSetAttribute(k_rb_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallCells * (int)sizeof(float));
+    cudaError_t e = launch_pdl(k_rb_small, dim3(B), dim3(kSmallThreads), smem, st, a, max_sweeps, check_every, tol, qoff,
+                               sweeps_out, res_out);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- Jacobi
 // Eq. 1: every free cell from the previous iterate, u <- 0.25 ((E + W) + (N + S)), read
 // from buffer cur[b] ^ lp and written to the other one (fixed cells copied through).  One sweep per
@@ -754,6 +845,7 @@ void preload_relax_kernels() {
     cudaFuncGetAttributes(&a, k_relax_init);
     cudaFuncGetAttributes(&a, k_fixup);
     cudaFuncGetAttributes(&a, k_res_group_max);
+    cudaFuncGetAttributes(&a, k_rb_small);
     cudaGetLastError();
 }
 

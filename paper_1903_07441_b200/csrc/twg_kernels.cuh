@@ -44,6 +44,9 @@ struct LexArgs {
 cudaError_t launch_lex(const LexArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_warp_map(int32_t* out, int W, int H, double cs, double ox, double oy, double xr, double yr, double c,
                             double s, double w, cudaStream_t st);
+bool small_grid(int W, int H);  // k_rb_small applies (the field fits in shared memory)
+cudaError_t launch_rb_small(const RelaxArgs& a, int B, int max_sweeps, int check_every, float tol, int qoff,
+                            int* sweeps_out, float* res_out, cudaStream_t st);
 cudaError_t launch_res_group_max(unsigned* const* ptrs, int n, int B, cudaStream_t st);
 cudaError_t launch_relax_init(int* done, int* sweeps, int* where, unsigned* res_bits, float* res, int B, cudaStream_t st);
 cudaError_t launch_check(int B, int* done, int* sweeps, unsigned* res_bits, float* res_final, int* where, int chunk,
