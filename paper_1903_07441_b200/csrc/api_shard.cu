@@ -19,6 +19,15 @@
 namespace twg {
 namespace host {
 
+// Stream-ordered device scratch released on every exit path.
+struct AsyncBuf {
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    ~AsyncBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
 static int owner_of(const twg_ctx* c, int gy) {
     const int n = c->shard.nranks, H = c->shard.H_global;
     const int base = H / n, extra = H % n;
@@ -47,9 +56,11 @@ twg_status sharded_extract_path(twg_ctx* c, const twg_band_cfg* cfg, int32_t* ce
         return fail(c, TWG_E_OUT_OF_BOUNDS, "robot cell outside the grid");
     int owner = owner_of(c, gy);
     // device scratch: [msg 4 | walk out 4 | segment cells 2 max_len | path 2 max_len]
-    int* d = nullptr;
+    AsyncBuf db;
+    db.st = st;
     const size_t nints = 8 + 4 * (size_t)max_len;
-    TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&d), nints * sizeof(int), st));
+    TWG_CUDA(c, cudaMallocAsync(&db.p, nints * sizeof(int), st));
+    int* d = static_cast<int*>(db.p);
     TWG_CUDA(c, cudaMemsetAsync(d, 0, nints * sizeof(int), st));
     int* msg = d;
     int* wout = d + 4;
@@ -87,8 +98,6 @@ twg_status sharded_extract_path(twg_ctx* c, const twg_band_cfg* cfg, int32_t* ce
         }
     }
     if (code != TWG_OK) {
-        TWG_CUDA(c, cudaFreeAsync(d, st));
-        TWG_CUDA(c, cudaStreamSynchronize(st));
         if (n_cells) *n_cells = 0;
         if (n_smooth) *n_smooth = 0;
         if (next_xy) {
@@ -114,8 +123,10 @@ twg_status sharded_extract_path(twg_ctx* c, const twg_band_cfg* cfg, int32_t* ce
     const int y0 = std::max(0, ymin - R), y1 = std::min(c->shard.H_global, ymax + R + 1);
     const int nrows = y1 - y0;
     const int64_t P = c->P;
-    unsigned* corr = nullptr;
-    TWG_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&corr), (size_t)nrows * P * sizeof(float), st));
+    AsyncBuf cb;
+    cb.st = st;
+    TWG_CUDA(c, cudaMallocAsync(&cb.p, (size_t)nrows * P * sizeof(float), st));
+    unsigned* corr = static_cast<unsigned*>(cb.p);
     TWG_CUDA(c, cudaMemsetAsync(corr, 0, (size_t)nrows * P * sizeof(float), st));
     for (twg_ctx* m : g) {  // owned rows of each slab inside [y0, y1)
         const int a = std::max(y0, m->shard.r0), e = std::min(y1, m->shard.r1);
@@ -185,9 +196,6 @@ twg_status sharded_extract_path(twg_ctx* c, const twg_band_cfg* cfg, int32_t* ce
         next_xy[0] = m.next_x;
         next_xy[1] = m.next_y + (float)y0;
     }
-    TWG_CUDA(c, cudaFreeAsync(corr, st));
-    TWG_CUDA(c, cudaFreeAsync(d, st));
-    TWG_CUDA(c, cudaStreamSynchronize(st));
     return m.n_smooth > cfg->max_smooth ? TWG_W_TRUNCATED : TWG_OK;
 }
 

@@ -440,69 +440,66 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
 // evaluated on the device after every check sweep -- the same operations as the tile kernel and the
 // oracle, without one launch (plus one k_check) per chunk.  The result is written back in place.
 constexpr int kSmallCells = 40960;  // 160 KiB of shared memory
-constexpr int kSmallThreads = 1024;
+constexpr int kSmallThreads = 1024;  // 32 warps: rows are dealt to warps round robin, lanes stride a row
 
 __global__ void __launch_bounds__(kSmallThreads) k_rb_small(RelaxArgs a, int max_sweeps, int check_every, float tol,
                                                             int qoff, int* __restrict__ sweeps_out,
                                                             float* __restrict__ res_out) {
     extern __shared__ float sf[];  // [H][W]
-    __shared__ unsigned s_red[32];
-    __shared__ int s_stop;
+    __shared__ unsigned s_red[kSmallThreads / 32];
     pdl_wait();
     pdl_trigger();
     const int b = blockIdx.x;
     if (a.done[b]) return;
     const int W = a.W, H = a.H, n = W * H;
     float* g = (a.cur[b] ? a.u1 : a.u0) + (int64_t)b * a.sstride;
-    for (int q = threadIdx.x; q < n; q += blockDim.x) sf[q] = g[(int64_t)(q / W) * a.P + q % W];
-    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NWARP = kSmallThreads / 32;
+    for (int y = wid; y < H; y += NWARP)
+        for (int x = lane; x < W; x += 32) sf[y * W + x] = g[(int64_t)y * a.P + x];
+    __syncthreads();
     float res = 0.0f;
     int s = 0;
     for (s = 1; s <= max_sweeps; ++s) {
         const bool check = (s % check_every == 0) || s == max_sweeps;
         float dmax = 0.0f;
+#pragma unroll 1
         for (int color = 0; color < 2; ++color) {
-            // cells of this colour: (x + row_offset + y) & 1 == color, i.e. x = 2 j + ((color + qoff + y) & 1)
-            const int half = (W + 1) / 2;
-            for (int t = threadIdx.x; t < half * H; t += blockDim.x) {
-                const int y = t / half;
-                const int x = 2 * (t - y * half) + ((color + qoff + y) & 1);
-                if (x >= W) continue;
-                const int q = y * W + x;
-                const float c = sf[q];
-                if (!is_free(c)) continue;
-                const float e = x + 1 < W ? fabsf(sf[q + 1]) : 0.0f;
-                const float w = x > 0 ? fabsf(sf[q - 1]) : 0.0f;
-                const float nn = y > 0 ? fabsf(sf[q - W]) : 0.0f;
-                const float ss = y + 1 < H ? fabsf(sf[q + W]) : 0.0f;
-                const float nv = 0.25f * ((e + w) + (nn + ss));
-                if (check && y >= a.res_r0 && y < a.res_r1) dmax = fmaxf(dmax, fabsf(-nv - c));
-                sf[q] = -nv;
+            for (int y = wid; y < H; y += NWARP) {
+                // cells of this colour in row y: (x + row_offset + y) & 1 == color
+                const int x0 = (color + qoff + y) & 1;
+                const bool cnt = check && y >= a.res_r0 && y < a.res_r1;
+                float* row = sf + y * W;
+                for (int x = x0 + 2 * lane; x < W; x += 64) {
+                    const float c = row[x];
+                    if (!is_free(c)) continue;
+                    const float e = x + 1 < W ? fabsf(row[x + 1]) : 0.0f;
+                    const float w = x > 0 ? fabsf(row[x - 1]) : 0.0f;
+                    const float nn = y > 0 ? fabsf(row[x - W]) : 0.0f;
+                    const float ss = y + 1 < H ? fabsf(row[x + W]) : 0.0f;
+                    const float nv = 0.25f * ((e + w) + (nn + ss));
+                    if (cnt) dmax = fmaxf(dmax, fabsf(-nv - c));
+                    row[x] = -nv;
+                }
             }
             __syncthreads();
         }
         if (check) {
-            unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(dmax));
+            const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(dmax));
             if (lane == 0) s_red[wid] = m;
             __syncthreads();
-            if (wid == 0) {
-                m = lane < (int)(blockDim.x >> 5) ? s_red[lane] : 0u;
-                m = __reduce_max_sync(0xffffffffu, m);
-                if (lane == 0) {
-                    res = __uint_as_float(m);
-                    s_stop = ((s % check_every == 0 && res < tol) || s == max_sweeps) ? 1 : 0;
-                    s_red[0] = m;
-                }
-            }
-            __syncthreads();
-            res = __uint_as_float(s_red[0]);
-            if (s_stop) break;
-            __syncthreads();  // s_red / s_stop are rewritten at the next check
+            unsigned mm = 0u;
+#pragma unroll
+            for (int k = 0; k < NWARP; ++k) mm = max(mm, s_red[k]);
+            res = __uint_as_float(mm);
+            __syncthreads();  // s_red is rewritten at the next check
+            if ((s % check_every == 0 && res < tol) || s == max_sweeps) break;
         }
     }
     if (s > max_sweeps) s = max_sweeps;
-    for (int q = threadIdx.x; q < n; q += blockDim.x) g[(int64_t)(q / W) * a.P + q % W] = sf[q];
+    (void)n;
+    for (int y = wid; y < H; y += NWARP)
+        for (int x = lane; x < W; x += 32) g[(int64_t)y * a.P + x] = sf[y * W + x];
     if (threadIdx.x == 0) {
         sweeps_out[b] = s;
         res_out[b] = res;
