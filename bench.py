@@ -656,6 +656,16 @@ def _launch_ranks(args) -> int:
     return subprocess.call(cmd)
 
 
+def _json_stdout():
+    """Keep stdout for the one JSON line: native libraries write to file descriptor 1 (NCCL's version
+    banner when the row-slab communicator is created), so fd 1 is pointed at stderr for the run and
+    Python's stdout writes to a saved copy of the original descriptor."""
+    sys.stdout.flush()
+    fd = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(fd, "w", buffering=1)
+
+
 def main():
     args = _args()
     ws_env = os.environ.get("WORLD_SIZE")
@@ -669,6 +679,7 @@ def main():
         print(json.dumps({"probe": True, "rank": rank, "world_size": ws, "local_rank": local, "pid": os.getpid()}),
               flush=True)
         return
+    _json_stdout()
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "c4":
