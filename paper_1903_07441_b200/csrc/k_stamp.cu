@@ -306,6 +306,11 @@ void preload_stamp_kernels() {
     cudaGetLastError();
 }
 
+// Threads per footprint CTA of k_unstamp / k_stamp: a few scenarios (C3: 200 tracks, a fresh track's
+// footprint ~1850 cells) fill the GPU only with wide CTAs; a batch (C5: 1024 x 20 footprints of ~120
+// cells, the CTA loops over its box) with narrow ones -- 1024-thread CTAs there mostly idle.
+static int box_threads(int nscen, int wide) { return nscen > 8 ? 128 : wide; }
+
 cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_tracks, int any_cold, int* n_launch,
                           cudaStream_t st) {
     int nl = 0;
@@ -316,14 +321,14 @@ cudaError_t launch_encode(const EncodeArgs& e, int max_prev_boxes, int max_track
         ++nl;
     }
     if (max_prev_boxes > 0) {
-        if (cudaError_t err = launch_pdl(k_unstamp, dim3(max_prev_boxes, e.nscen), dim3(1024), 0, st, e)) return err;
+        if (cudaError_t err = launch_pdl(k_unstamp, dim3(max_prev_boxes, e.nscen), dim3(box_threads(e.nscen, 1024)), 0, st, e)) return err;
         ++nl;
     }
     const int sb = (e.nscen + 127) / 128;
     if (max_tracks > 0) {  // the goal reset / set ride on the first CTA of each scenario
         if (cudaError_t err = launch_pdl(k_track_predict, dim3((max_tracks + 63) / 64, e.nscen), dim3(64), 0, st, e))
             return err;
-        if (cudaError_t err = launch_pdl(k_stamp, dim3(max_tracks, e.nscen), dim3(512), 0, st, e)) return err;
+        if (cudaError_t err = launch_pdl(k_stamp, dim3(max_tracks, e.nscen), dim3(box_threads(e.nscen, 512)), 0, st, e)) return err;
         nl += 2;
     } else {
         if (cudaError_t err = launch_pdl(k_goal_reset, dim3(sb), dim3(128), 0, st, e)) return err;
