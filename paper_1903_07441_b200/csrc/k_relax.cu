@@ -205,9 +205,12 @@ __device__ __forceinline__ void hs_fast(FRow& c, const FRow& up, const FRow& dn,
 // residual sweeps, |du| of the owned rows.
 // `upr`: the row above (slot of row i - K - 1), passed separately because for K = 2T that slot may
 // already hold the next row (the interleaved order below loads row S + 1 early).
-template <int T, int QOFF, bool RESID, bool GOAL, int S, int K>
+// FIRST: the segment's first block, whose half-sweep k of step S only touches rows above every row
+// the stored rows depend on when 2k > S (those rows are never read by a needed update) -- skipped.
+template <int T, int QOFF, bool RESID, bool GOAL, bool FIRST, int S, int K>
 __device__ __forceinline__ void fast_hs(FRow (&win)[2 * T + 2], const FRow& upr, int i, const Strip& st,
                                         float& dmax) {
+    if constexpr (FIRST && 2 * K > S) return;
     constexpr int NW = 2 * T + 2;
     constexpr int Qp = (S + 1 + QOFF) & 1;
     constexpr int c = (S - K + 2 * NW) % NW, dn = (S - K + 1 + 2 * NW) % NW;
@@ -261,32 +264,32 @@ __device__ __forceinline__ void fast_store(FRow (&win)[2 * T + 2], int i, Strip&
 // Steps S and S + 1 with their half-sweeps interleaved along the anti-diagonals of the wavefront:
 // (S, k) needs (S, k - 1), (S - 1, k - 1) and (S - 2, k - 1) only, so (S, k) and (S + 1, k - 1) are
 // independent and issue back to back -- two dependency chains per warp instead of one.
-template <int T, int QOFF, bool RESID, bool GOAL, int S, int K>
+template <int T, int QOFF, bool RESID, bool GOAL, bool FIRST, int S, int K>
 __device__ __forceinline__ void fast_pair_hs(FRow (&win)[2 * T + 2], const FRow& last_up, int ib, const Strip& st,
                                              float& dmax) {
     if constexpr (K <= 2 * T) {
-        if constexpr (K == 2 * T) fast_hs<T, QOFF, RESID, GOAL, S, K>(win, last_up, ib + S, st, dmax);
-        else fast_hs<T, QOFF, RESID, GOAL, S, K>(win, up_of<T, S, K>(win), ib + S, st, dmax);
-        fast_hs<T, QOFF, RESID, GOAL, S + 1, K - 1>(win, up_of<T, S + 1, K - 1>(win), ib + S + 1, st, dmax);
-        fast_pair_hs<T, QOFF, RESID, GOAL, S, K + 1>(win, last_up, ib, st, dmax);
+        if constexpr (K == 2 * T) fast_hs<T, QOFF, RESID, GOAL, FIRST, S, K>(win, last_up, ib + S, st, dmax);
+        else fast_hs<T, QOFF, RESID, GOAL, FIRST, S, K>(win, up_of<T, S, K>(win), ib + S, st, dmax);
+        fast_hs<T, QOFF, RESID, GOAL, FIRST, S + 1, K - 1>(win, up_of<T, S + 1, K - 1>(win), ib + S + 1, st, dmax);
+        fast_pair_hs<T, QOFF, RESID, GOAL, FIRST, S, K + 1>(win, last_up, ib, st, dmax);
     }
 }
 
-template <int T, int QOFF, bool RESID, bool GOAL, int S>
+template <int T, int QOFF, bool RESID, bool GOAL, bool FIRST, int S>
 __device__ __forceinline__ void block_steps_fast(FRow (&win)[2 * T + 2], int ib, Strip& st) {
     constexpr int NW = 2 * T + 2;
     float dmax = st.dmax;
     fast_load<T, GOAL, S>(win, st);
-    fast_hs<T, QOFF, RESID, GOAL, S, 1>(win, up_of<T, S, 1>(win), ib + S, st, dmax);
+    fast_hs<T, QOFF, RESID, GOAL, FIRST, S, 1>(win, up_of<T, S, 1>(win), ib + S, st, dmax);
     // row S + 1 lands in the slot of row S - 2T - 1, which (S, 2T) still reads as its upper neighbour
     const FRow last_up = win[(S + 1) % NW];
     fast_load<T, GOAL, S + 1>(win, st);
-    fast_pair_hs<T, QOFF, RESID, GOAL, S, 2>(win, last_up, ib, st, dmax);
+    fast_pair_hs<T, QOFF, RESID, GOAL, FIRST, S, 2>(win, last_up, ib, st, dmax);
     fast_store<T, S>(win, ib + S, st);
-    fast_hs<T, QOFF, RESID, GOAL, S + 1, 2 * T>(win, up_of<T, S + 1, 2 * T>(win), ib + S + 1, st, dmax);
+    fast_hs<T, QOFF, RESID, GOAL, FIRST, S + 1, 2 * T>(win, up_of<T, S + 1, 2 * T>(win), ib + S + 1, st, dmax);
     fast_store<T, S + 1>(win, ib + S + 1, st);
     st.dmax = dmax;
-    if constexpr (S + 2 < 2 * T + 2) block_steps_fast<T, QOFF, RESID, GOAL, S + 2>(win, ib, st);
+    if constexpr (S + 2 < 2 * T + 2) block_steps_fast<T, QOFF, RESID, GOAL, FIRST, S + 2>(win, ib, st);
 }
 
 // The fast path's row loop.  has_goal: the goal cell lies in the warp's region; it is loaded at step
@@ -309,11 +312,13 @@ __device__ __forceinline__ void fast_rows(float* ring, uint64_t* bars, const CUt
         mbar_wait(&bars[sg], (blk / kStages) & 1);
         st.rows = ring + sg * STAGE_F;
         const bool gblk = has_goal && blk * NW <= i0 + 2 * T && blk * NW + NW - 1 >= i0;
-        // The segment's first block runs the steady body too: skipping its half-sweeps 2k > S (rows above
-        // every row the stored rows depend on) saves ~4 % of the updates but a second 14-step body in the
-        // instruction caches cost more (measured: 33.3 -> 32.6 us per T = 6 launch without it).
-        if (gblk) block_steps_fast<T, QOFF, RESID, true, 0>(win, blk * NW, st);
-        else block_steps_fast<T, QOFF, RESID, false, 0>(win, blk * NW, st);
+        if (blk == 0) {
+            if (gblk) block_steps_fast<T, QOFF, RESID, true, true, 0>(win, 0, st);
+            else block_steps_fast<T, QOFF, RESID, false, true, 0>(win, 0, st);
+        } else {
+            if (gblk) block_steps_fast<T, QOFF, RESID, true, false, 0>(win, blk * NW, st);
+            else block_steps_fast<T, QOFF, RESID, false, false, 0>(win, blk * NW, st);
+        }
         if (blk + kStages < nblk) {
             __syncwarp();
             if (st.lane == 0) {
