@@ -13,6 +13,8 @@ def test_reference_arm_json_line():
                           "--warmup", "3", "--size", "256", "--obstacles", "10"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
+    # stdout carries the JSON line only (bench.py points fd 1 at stderr for native libraries' output)
+    assert len(out.stdout.strip().splitlines()) == 1, out.stdout[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
