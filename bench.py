@@ -329,16 +329,33 @@ def run_ours(args):
         # the two configurations that shard, measured in the same job at the same N so
         # that the driver's 1/2/4/8 runs carry their scaling too
         def sub(name, fn):  # a failing sub-result is reported in the line, it does not lose the C3 line
+            pending[0] = name
             try:
                 out[name] = fn()
             except Exception as e:  # noqa: BLE001
                 out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
 
+        # watchdog: a sub-result that does not finish (e.g. a collective that never completes on some
+        # multi-GPU topology) must not cost the C3 line -- after SUB_LIMIT_S every rank stops, rank 0
+        # first printing the line with the pending sub-result marked
+        import threading
+        pending = [None]
+
+        def _expired():
+            if rank == 0:
+                out[pending[0] or "sub"] = {"error": f"did not finish within {SUB_LIMIT_S} s"}
+                print(json.dumps(out), flush=True)
+            os._exit(0)
+
+        dog = threading.Timer(SUB_LIMIT_S, _expired)
+        dog.daemon = True
+        dog.start()
         sub("c4_slab", lambda: c4_slab(args, dev, ws, rank, local))
         sub("c5_batch", lambda: c5_batch(args, dev, ws, rank, local))
         if rank == 0:  # single-GPU configurations (BASELINE configs[0], [1])
             sub("c1_solve", lambda: c1_solve(args, dev, not args.no_cpu_baseline))
             sub("c2_loop", lambda: c2_loop(args, dev, not args.no_cpu_baseline))
+        dog.cancel()
     if rank == 0 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
@@ -654,6 +671,9 @@ def _launch_ranks(args) -> int:
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd)
+
+
+SUB_LIMIT_S = 240  # bound on the sub-results of the default line (normally well under a minute)
 
 
 def _json_stdout():
