@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_rb_tblock(const __grid_co
 // evaluated on the device after every check sweep -- the same operations as the tile kernel and the
 // oracle, without one launch (plus one k_check) per chunk.  The result is written back in place.
 constexpr int kSmallCells = 40960;  // 160 KiB of shared memory
-constexpr int kSmallThreads = 1024;  // 32 warps: rows are dealt to warps round robin, lanes stride a row
+constexpr int kSmallThreads = 1024;  // 32 warps (measured: 512 / 256 threads 7 % / 64 % slower on C1)
 
 __global__ void __launch_bounds__(kSmallThreads) k_rb_small(RelaxArgs a, int max_sweeps, int check_every, float tol,
                                                             int qoff, int* __restrict__ sweeps_out,
@@ -465,21 +465,39 @@ __global__ void __launch_bounds__(kSmallThreads) k_rb_small(RelaxArgs a, int max
         float dmax = 0.0f;
 #pragma unroll 1
         for (int color = 0; color < 2; ++color) {
-            for (int y = wid; y < H; y += NWARP) {
+            // rows y and y + NWARP together (same colour offset: NWARP is even), every load of both issued
+            // before any store -- cells of one colour never neighbour each other, so the stores cannot
+            // feed the loads of the same pass
+            for (int y = wid; y < H; y += 2 * NWARP) {
                 // cells of this colour in row y: (x + row_offset + y) & 1 == color
                 const int x0 = (color + qoff + y) & 1;
-                const bool cnt = check && y >= a.res_r0 && y < a.res_r1;
-                float* row = sf + y * W;
+                const int y2 = y + NWARP;
+                const bool has2 = y2 < H;
+                const bool cnt1 = check && y >= a.res_r0 && y < a.res_r1;
+                const bool cnt2 = check && has2 && y2 >= a.res_r0 && y2 < a.res_r1;
+                float* row1 = sf + y * W;
+                float* row2 = sf + (has2 ? y2 : y) * W;
                 for (int x = x0 + 2 * lane; x < W; x += 64) {
-                    const float c = row[x];
-                    if (!is_free(c)) continue;
-                    const float e = x + 1 < W ? fabsf(row[x + 1]) : 0.0f;
-                    const float w = x > 0 ? fabsf(row[x - 1]) : 0.0f;
-                    const float nn = y > 0 ? fabsf(row[x - W]) : 0.0f;
-                    const float ss = y + 1 < H ? fabsf(row[x + W]) : 0.0f;
-                    const float nv = 0.25f * ((e + w) + (nn + ss));
-                    if (cnt) dmax = fmaxf(dmax, fabsf(-nv - c));
-                    row[x] = -nv;
+                    const float c1 = row1[x];
+                    const float e1 = x + 1 < W ? fabsf(row1[x + 1]) : 0.0f;
+                    const float w1 = x > 0 ? fabsf(row1[x - 1]) : 0.0f;
+                    const float n1 = y > 0 ? fabsf(row1[x - W]) : 0.0f;
+                    const float s1 = y + 1 < H ? fabsf(row1[x + W]) : 0.0f;
+                    const float c2 = row2[x];
+                    const float e2 = x + 1 < W ? fabsf(row2[x + 1]) : 0.0f;
+                    const float w2 = x > 0 ? fabsf(row2[x - 1]) : 0.0f;
+                    const float n2 = has2 ? fabsf(row2[x - W]) : 0.0f;  // y2 >= NWARP > 0
+                    const float s2 = y2 + 1 < H ? fabsf(row2[x + W]) : 0.0f;
+                    const float nv1 = 0.25f * ((e1 + w1) + (n1 + s1));
+                    const float nv2 = 0.25f * ((e2 + w2) + (n2 + s2));
+                    if (is_free(c1)) {
+                        if (cnt1) dmax = fmaxf(dmax, fabsf(-nv1 - c1));
+                        row1[x] = -nv1;
+                    }
+                    if (has2 && is_free(c2)) {
+                        if (cnt2) dmax = fmaxf(dmax, fabsf(-nv2 - c2));
+                        row2[x] = -nv2;
+                    }
                 }
             }
             __syncthreads();
@@ -488,9 +506,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_rb_small(RelaxArgs a, int max
             const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(dmax));
             if (lane == 0) s_red[wid] = m;
             __syncthreads();
-            unsigned mm = 0u;
-#pragma unroll
-            for (int k = 0; k < NWARP; ++k) mm = max(mm, s_red[k]);
+            // every warp reduces the warp maxima itself (one shared load per lane and a warp max), so the
+            // block needs no second round trip through shared memory
+            const unsigned mm = __reduce_max_sync(0xffffffffu, lane < NWARP ? s_red[lane] : 0u);
             res = __uint_as_float(mm);
             __syncthreads();  // s_red is rewritten at the next check
             if ((s % check_every == 0 && res < tol) || s == max_sweeps) break;
