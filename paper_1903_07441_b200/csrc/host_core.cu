@@ -360,8 +360,9 @@ twg_status encode(twg_ctx* c, const std::vector<EncodeReq>& reqs, const twg_trac
 // Output rows per warp (hseg).  hseg + 4T is a multiple of NW = 2T + 2 (the kernel streams whole
 // NW-row blocks, so any other value pays for padded rows) and even (the colour parity of the first
 // row is a compile-time constant).  Among those, pick the one minimising the load model measured on
-// B200: a launch takes ~ (CTAs on the busiest SM) x (hseg + 4T) /
-// min(CTAs per SM, 2) -- throughput saturates at two 4-warp CTAs per SM.
+// B200: the CTAs run in waves of the kernel's occupancy (CTAs resident per
+// SM), and a wave of n CTAs takes ~ (hseg + 4T) x max(1, n warps / 8) -- throughput saturates at eight
+// warps per SM (one 8-warp CTA at T = 6, 198 registers).
 int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows, int n_sm) {
     const int NW = 2 * T + 2;
     if (cfg_rows > 0) {
@@ -369,6 +370,7 @@ int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows, int n_sm) {
         h = (h + 1) & ~1;
         return std::max(h, 2);
     }
+    const int resident = std::max(1, rb_tblock_ctas_per_sm(T));
     int best_h = 2;
     double best = 1e300;
     for (int k = 1; k <= 256; ++k) {
@@ -378,7 +380,9 @@ int auto_hseg(int T, int H, int n_strips, int nscen, int cfg_rows, int n_sm) {
         const long long segs = (H + hh - 1) / hh;
         const long long ctas = (segs * n_strips * nscen + kWarpsPerCta - 1) / kWarpsPerCta;
         const long long per_sm = (ctas + n_sm - 1) / n_sm;
-        const double cost = (double)per_sm * (hh + 4 * T) / (double)std::min<long long>(per_sm, 2);
+        double cost = 0.0;
+        for (long long left = per_sm; left > 0; left -= resident)
+            cost += (double)(hh + 4 * T) * std::max(1.0, (double)std::min<long long>(left, resident) * kWarpsPerCta / 8.0);
         if (cost < best * 0.999) {
             best = cost;
             best_h = hh;

@@ -817,6 +817,37 @@ static cudaError_t launch_T(const CUtensorMap& m0, const CUtensorMap& m1, const 
     return cudaGetLastError();
 }
 
+// CTAs of k_rb_tblock<T> resident per SM (registers, shared memory), per process.
+template <int T>
+static int ctas_per_sm_T() {
+    static int n = -1;
+    if (n < 0) {
+        const size_t smem = (size_t)kWarpsPerCta * kStages * (2 * T + 2) * kStripW * 4 + kWarpsPerCta * kStages * sizeof(uint64_t);
+        cudaFuncSetAttribute(k_rb_tblock<T, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int k = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, k_rb_tblock<T, 0, false>, kWarpsPerCta * 32, smem) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            k = 1;
+        }
+        n = std::max(k, 1);
+    }
+    return n;
+}
+
+int rb_tblock_ctas_per_sm(int T) {
+    switch (T) {
+        case 1: return ctas_per_sm_T<1>();
+        case 2: return ctas_per_sm_T<2>();
+        case 3: return ctas_per_sm_T<3>();
+        case 4: return ctas_per_sm_T<4>();
+        case 5: return ctas_per_sm_T<5>();
+        case 6: return ctas_per_sm_T<6>();
+        case 7: return ctas_per_sm_T<7>();
+        default: return ctas_per_sm_T<8>();
+    }
+}
+
 template <int T>
 static cudaError_t launch_T3(const CUtensorMap& m0, const CUtensorMap& m1, const RelaxArgs& a, int B, int qoff, bool resid,
                              cudaStream_t st) {

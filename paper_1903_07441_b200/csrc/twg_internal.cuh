@@ -22,7 +22,10 @@ namespace twg {
 // stages of NW = 2T + 2 rows (one TMA box = one unrolled block of the row loop);
 // the 2T half-sweeps of T red-black sweeps run as a register wavefront
 // (DESIGN.md "k_rb_tblock").
-constexpr int kWarpsPerCta = 4;
+#ifndef TWG_RELAX_WARPS
+#define TWG_RELAX_WARPS 8
+#endif
+constexpr int kWarpsPerCta = TWG_RELAX_WARPS;  // 8: one CTA per SM at T = 6 (198 registers)
 constexpr int kStripW = 128;
 #ifndef TWG_RELAX_STAGES
 #define TWG_RELAX_STAGES 2

@@ -24,6 +24,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 // k_relax.cu (rows a4-a6)
 cudaError_t launch_rb_tblock(int T, const CUtensorMap& map0, const CUtensorMap& map1, const RelaxArgs& a, int B, int qoff, bool resid,
                              cudaStream_t st);
+int rb_tblock_ctas_per_sm(int T);  // CTAs of k_rb_tblock<T> resident per SM (occupancy)
 cudaError_t launch_jacobi(const RelaxArgs& a, int B, bool resid, cudaStream_t st);
 struct LexArgs {
     float* u0;
