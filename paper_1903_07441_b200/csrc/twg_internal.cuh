@@ -28,7 +28,7 @@ namespace twg {
 constexpr int kWarpsPerCta = TWG_RELAX_WARPS;  // 8: one CTA per SM at T = 6 (198 registers)
 constexpr int kStripW = 128;
 #ifndef TWG_RELAX_STAGES
-#define TWG_RELAX_STAGES 2
+#define TWG_RELAX_STAGES 3
 #endif
 constexpr int kStages = TWG_RELAX_STAGES;
 constexpr int kMaxT = 8;
